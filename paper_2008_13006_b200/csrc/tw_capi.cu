@@ -1,0 +1,290 @@
+// C ABI (include/tw_b200.h): plan upload, TMA descriptor creation and the
+// launch wrappers of libtw_b200.so.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tw_internal.h"
+
+namespace tw {
+cudaError_t launch_tw_gemm_sm100(const CUtensorMap &tmap, const GemmArgs &args, int out_dtype, int grid,
+                                 cudaStream_t stream);
+cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
+                        cudaStream_t s);
+cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t lda, int64_t col_begin, int64_t n_cols,
+                        const int32_t *cp, const int32_t *ri, const float *va, void *ct, int64_t ldc, int out_dtype,
+                        int accumulate, cudaStream_t s);
+cudaError_t launch_exact(const tw_plan *p, const float *at, int64_t m, int64_t lda, float *ct, int64_t ldc,
+                         cudaStream_t s);
+
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return fail(TW_ERR_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int sm_count_of_current(int *sms, int *major) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  static int cache_sms[64] = {0}, cache_major[64] = {0};
+  if (dev < 64 && cache_sms[dev]) {
+    *sms = cache_sms[dev];
+    *major = cache_major[dev];
+    return TW_OK;
+  }
+  int s = 0, mj = 0;
+  if ((e = cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+    return cuda_fail(e, "cudaDeviceGetAttribute");
+  if ((e = cudaDeviceGetAttribute(&mj, cudaDevAttrComputeCapabilityMajor, dev)) != cudaSuccess)
+    return cuda_fail(e, "cudaDeviceGetAttribute");
+  if (dev < 64) { cache_sms[dev] = s; cache_major[dev] = mj; }
+  *sms = s;
+  *major = mj;
+  return TW_OK;
+}
+
+int require_sm100(int *sms) {
+  int major = 0;
+  int rc = sm_count_of_current(sms, &major);
+  if (rc) return rc;
+  if (major != 10) return fail(TW_ERR_CUDA, "libtw_b200 requires an sm_100 (B200) device; found compute capability " +
+                                                std::to_string(major) + ".x");
+  return TW_OK;
+}
+
+template <typename T>
+int upload(T **dst, const std::vector<T> &src) {
+  *dst = nullptr;
+  if (src.empty()) return TW_OK;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void **>(dst), src.size() * sizeof(T));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy");
+  return TW_OK;
+}
+
+int out_size(int dtype) { return dtype == TW_F32 ? 4 : 2; }
+
+}  // namespace
+}  // namespace tw
+
+using namespace tw;
+
+extern "C" {
+
+int tw_device_sm_count(int *sms) {
+  int major = 0;
+  return sm_count_of_current(sms, &major);
+}
+
+int tw_plan_create(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off, const int32_t *col_ids,
+                   const uint32_t *row_mask_words, const float *subs, const int64_t *sub_off, int in_dtype,
+                   int64_t col_begin, int64_t col_end, tw_plan **out) {
+  clear_error();
+  if (!out) return fail(TW_ERR_ARG, "null out");
+  *out = nullptr;
+  tw_plan *p = new (std::nothrow) tw_plan();
+  if (!p) return fail(TW_ERR_NOMEM, "out of host memory");
+  int rc = build_host_plan(k, n, g, n_tiles, col_off, col_ids, row_mask_words, subs, sub_off, in_dtype, col_begin,
+                           col_end, p->host);
+  if (rc) { delete p; return rc; }
+  cudaGetDevice(&p->device);
+  if ((rc = upload(&p->d_tiles, p->host.tiles)) || (rc = upload(&p->d_kidx, p->host.kidx)) ||
+      (rc = upload(&p->d_colids, p->host.colids)) || (rc = upload(&p->d_zero, p->host.zero_rows)) ||
+      (rc = upload(&p->d_wimg, p->host.wimg))) {
+    tw_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return TW_OK;
+}
+
+int tw_plan_build_host(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,
+                       const int32_t *col_ids, const uint32_t *row_mask_words, const float *subs,
+                       const int64_t *sub_off, int in_dtype, int64_t col_begin, int64_t col_end, tw_plan **out) {
+  clear_error();
+  if (!out) return fail(TW_ERR_ARG, "null out");
+  *out = nullptr;
+  tw_plan *p = new (std::nothrow) tw_plan();
+  if (!p) return fail(TW_ERR_NOMEM, "out of host memory");
+  p->device = -1;
+  int rc = build_host_plan(k, n, g, n_tiles, col_off, col_ids, row_mask_words, subs, sub_off, in_dtype, col_begin,
+                           col_end, p->host);
+  if (rc) { delete p; return rc; }
+  *out = p;
+  return TW_OK;
+}
+
+int tw_plan_destroy(tw_plan *p) {
+  if (!p) return TW_OK;
+  if (p->device < 0) { delete p; return TW_OK; }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != p->device) cudaSetDevice(p->device);
+  cudaFree(p->d_tiles);
+  cudaFree(p->d_kidx);
+  cudaFree(p->d_colids);
+  cudaFree(p->d_zero);
+  cudaFree(p->d_wimg);
+  if (prev != p->device) cudaSetDevice(prev);
+  delete p;
+  return TW_OK;
+}
+
+int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
+            int accumulate, void *stream) {
+  clear_error();
+  if (!p) return fail(TW_ERR_ARG, "null plan");
+  if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan (tw_plan_build_host) cannot run on the GPU");
+  if (out_dtype != TW_F32 && out_dtype != TW_BF16 && out_dtype != TW_F16) return fail(TW_ERR_ARG, "bad out_dtype");
+  if (m < 0) return fail(TW_ERR_DIMENSION, "M must be >= 0");
+  if (m == 0) return TW_OK;
+  const HostPlan &hp = p->host;
+  const int64_t n_rows = hp.col_end - hp.col_begin;
+  if (n_rows == 0) return TW_OK;
+  if (m > (int64_t)1 << 30) return fail(TW_ERR_UNSUPPORTED, "M too large");
+  if (ldc < m) return fail(TW_ERR_DIMENSION, "ldc < M");
+  if (!ct) return fail(TW_ERR_ARG, "null output");
+  int sms = 0;
+  int rc = require_sm100(&sms);
+  if (rc) return rc;
+  const int64_t n_live = (int64_t)hp.tiles.size();
+  if (n_live > 0) {
+    if (!at) return fail(TW_ERR_ARG, "null activations");
+    if (lda < m) return fail(TW_ERR_DIMENSION, "lda < M");
+    if (lda % 8 != 0 || (reinterpret_cast<uintptr_t>(at) & 15) != 0)
+      return fail(TW_ERR_ARG, "activations need lda % 8 == 0 and a 16-byte aligned base (TMA)");
+  }
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (n_live > 0) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)hp.k};
+    cuuint64_t strides[1] = {(cuuint64_t)lda * 2};
+    cuuint32_t box[2] = {64, 1};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&tmap, hp.in_dtype == TW_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                     2, const_cast<void *>(at), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  }
+  GemmArgs a{};
+  a.tiles = p->d_tiles;
+  a.kidx = p->d_kidx;
+  a.colids = p->d_colids;
+  a.zero_rows = p->d_zero;
+  a.wimg = p->d_wimg;
+  a.out = ct;
+  a.ldc = ldc;
+  a.M = (int32_t)m;
+  a.n_live = (int32_t)n_live;
+  a.mblocks = (int32_t)((m + 127) / 128);
+  a.n_zero = accumulate ? 0 : (int32_t)hp.zero_rows.size();
+  a.accumulate = accumulate ? 1 : 0;
+  a.wbytes = hp.wrows * 128;
+  // kind::f16 instruction descriptor: D f32 [4,6)=1, A/B bf16 [7,10)/[10,13)=1
+  // (fp16 = 0), A MN-major [15]=1, B K-major [16]=0, M=128 -> [24,29)=8.
+  const uint32_t ab = hp.in_dtype == TW_BF16 ? 1u : 0u;
+  a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 15) | ((128u >> 4) << 24);
+  a.block_n = hp.block_n;
+  const int64_t units = n_live * a.mblocks;
+  const int64_t zero_bytes = (int64_t)a.n_zero * m * out_size(out_dtype);
+  int64_t grid = units;
+  const int64_t zero_ctas = (zero_bytes + (256 << 10) - 1) / (256 << 10);
+  if (zero_ctas > grid) grid = zero_ctas;
+  if (grid > sms) grid = sms;
+  if (grid < 1) grid = 1;
+  cudaError_t e = launch_tw_gemm_sm100(tmap, a, out_dtype, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tw_gemm launch");
+  return TW_OK;
+}
+
+int tw_gemm_exact(const tw_plan *p, const float *at, int64_t m, int64_t lda, float *ct, int64_t ldc, void *stream) {
+  clear_error();
+  if (!p) return fail(TW_ERR_ARG, "null plan");
+  if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan cannot run on the GPU");
+  if (m < 0 || lda < m || ldc < m) return fail(TW_ERR_DIMENSION, "bad M / lda / ldc");
+  int sms = 0;
+  int rc = require_sm100(&sms);
+  if (rc) return rc;
+  cudaError_t e = launch_exact(p, at, m, lda, ct, ldc, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tw_gemm_exact launch");
+  return TW_OK;
+}
+
+int tw_prep_activations(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
+                        void *stream) {
+  clear_error();
+  if (m < 0 || k < 0) return fail(TW_ERR_DIMENSION, "negative dims");
+  if (layout != TW_ROW_MAJOR && layout != TW_COL_MAJOR) return fail(TW_ERR_ARG, "bad layout");
+  if (ldat < m) return fail(TW_ERR_DIMENSION, "ldat < M");
+  if (m == 0 || k == 0) return TW_OK;
+  int sms = 0;
+  int rc = require_sm100(&sms);
+  if (rc) return rc;
+  cudaError_t e = launch_prep(a, m, k, layout, at, ldat, out_dtype, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tw_prep_activations launch");
+  return TW_OK;
+}
+
+int tw_spmm_csc(const void *at, int at_dtype, int64_t k, int64_t m, int64_t lda, int64_t n, const int32_t *col_ptr,
+                const int32_t *row_idx, const float *values, void *ct, int64_t ldc, int out_dtype, int accumulate,
+                void *stream) {
+  clear_error();
+  (void)k;
+  if (m < 0 || n < 0 || lda < m || ldc < m) return fail(TW_ERR_DIMENSION, "bad M / N / lda / ldc");
+  if (m == 0 || n == 0) return TW_OK;
+  int sms = 0;
+  int rc = require_sm100(&sms);
+  if (rc) return rc;
+  cudaError_t e = launch_spmm(at, at_dtype, m, lda, 0, n, col_ptr, row_idx, values, ct, ldc, out_dtype, accumulate,
+                              reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tw_spmm_csc launch");
+  return TW_OK;
+}
+
+int tw_gemm_tew(const tw_plan *p, const void *at, int64_t m, int64_t lda, const int32_t *col_ptr,
+                const int32_t *row_idx, const float *values, int64_t nnz, void *ct, int64_t ldc, int out_dtype,
+                void *stream) {
+  clear_error();
+  if (!p) return fail(TW_ERR_ARG, "null plan");
+  if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan cannot run on the GPU");
+  if (nnz == 0) return tw_gemm(p, at, m, lda, ct, ldc, out_dtype, 0, stream);  // engine.py:194-195
+  if (m == 0) return TW_OK;
+  const HostPlan &hp = p->host;
+  if (lda < m || ldc < m) return fail(TW_ERR_DIMENSION, "bad lda / ldc");
+  int sms = 0;
+  int rc = require_sm100(&sms);
+  if (rc) return rc;
+  // SpMM writes every row of the plan's column range (overlay covers pruned
+  // columns too, pruning.py:548-549); the TW kernel then adds into kept rows.
+  cudaError_t e = launch_spmm(at, hp.in_dtype, m, lda, hp.col_begin, hp.col_end - hp.col_begin, col_ptr, row_idx,
+                              values, ct, ldc, out_dtype, 0, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tw_gemm_tew spmm launch");
+  return tw_gemm(p, at, m, lda, ct, ldc, out_dtype, 1, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Internal declarations shared by the host packer, the C-ABI layer and the
+// CUDA launchers of libtw_b200.so.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "tw_b200.h"
+
+namespace tw {
+
+// thread-local error message behind tw_last_error()
+int fail(int code, const std::string &msg);
+void clear_error();
+
+// One live tile of a plan, in launch (LPT) order.  Mirrors a TileTask
+// (engine.py:24-37): the kept-K index list is `kidx[kidx_off .. +nkb*64)`
+// (padded with K, which the TMA gather treats as out of bounds -> zeros),
+// the output rows are `colids[col_off .. +n_i)` (re-based to the plan's
+// column range), the weight image is `wimg + w_off` (nkb blocks of
+// wrows x 128 B, pre-swizzled for the SW128 K-major UMMA operand).
+struct TileMeta {
+  int32_t kidx_off;
+  int32_t col_off;
+  int32_t n_i;
+  int32_t k16;      // ceil(k_i / 16): MMA k-steps
+  int64_t w_off;    // byte offset into the weight image
+  int32_t nkb;      // ceil(k_i / 64): pipeline stages
+  int32_t k_i;
+};
+static_assert(sizeof(TileMeta) == 32, "TileMeta layout");
+
+struct HostPlan {
+  int64_t k = 0, n = 0, g = 0;
+  int64_t col_begin = 0, col_end = 0;
+  int64_t n_tiles = 0;
+  int in_dtype = TW_BF16;
+  int block_n = 128;   // MMA N tile / TMEM columns per accumulator
+  int wrows = 128;     // weight-image rows per k-block (multiple of 16, <= block_n)
+  std::vector<TileMeta> tiles;        // live tiles, LPT order
+  std::vector<int32_t> src_tile;      // reference tile index of each live tile
+  std::vector<int32_t> kidx;          // padded kept-K lists
+  std::vector<int32_t> colids;        // block_n entries per live tile (-1 padded)
+  std::vector<int32_t> zero_rows;     // output rows written as zeros
+  std::vector<uint8_t> wimg;          // swizzled 16-bit weight image
+  int64_t kept_elems = 0, union_k = 0, sum_k = 0, sum_n = 0;
+};
+
+// Kernel arguments of the persistent TW-GEMM (tw_gemm_sm100.cu).
+struct GemmArgs {
+  const TileMeta *tiles;
+  const int32_t *kidx;
+  const int32_t *colids;
+  const int32_t *zero_rows;
+  const uint8_t *wimg;
+  void *out;
+  int64_t ldc;
+  int32_t M;
+  int32_t n_live;
+  int32_t mblocks;
+  int32_t n_zero;
+  int32_t accumulate;
+  int32_t wbytes;     // weight-image bytes per k-block (wrows * 128)
+  uint32_t idesc;     // instruction descriptor without the N field
+  int32_t block_n;
+};
+
+int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,
+                    const int32_t *col_ids, const uint32_t *row_mask_words, const float *subs,
+                    const int64_t *sub_off, int in_dtype, int64_t col_begin, int64_t col_end,
+                    HostPlan &hp);
+
+uint16_t f32_to_bf16_rne(float f);
+uint16_t f32_to_f16_rne(float f);
+
+}  // namespace tw
+
+// Device side of a plan (defined in tw_capi.cu).
+struct tw_plan {
+  tw::HostPlan host;
+  int device = 0;
+  tw::TileMeta *d_tiles = nullptr;
+  int32_t *d_kidx = nullptr;
+  int32_t *d_colids = nullptr;
+  int32_t *d_zero = nullptr;
+  uint8_t *d_wimg = nullptr;
+};

@@ -1,0 +1,281 @@
+"""GPU parity: libtw_b200.so (sm_100a) against the CPU oracle and the golden
+fixtures generated from the reference.  Marked `gpu`; run on a B200.
+
+Tolerances (north_star): GEMM outputs within rel-L2 <= 1e-3 of the reference
+computed in fp32 on identically bf16-rounded inputs; masks / indices /
+layouts bit-exact; pruned columns exactly 0.  The CUDA-core kernels
+(tw_gemm_exact, the SpMM) reproduce the reference's fp32 rounding sequence
+and are checked bit-exactly.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2008_13006_b200 as tw  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+from tests import golden_io as gio  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-3  # rel-L2 bar from north_star
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    assert torch.cuda.get_device_capability()[0] == 10, "sm_100 (B200) required"
+
+
+def to_tw_pattern(p):
+    k, n, g, tiles = p
+    return tw.TilePattern(k, n, g, tuple(tw.Tile(c, keep) for c, keep in tiles))
+
+
+def device_at(a: np.ndarray, dtype=torch.bfloat16):
+    """A (M x K fp32) -> A^T (K x M) on device via the product prep kernel."""
+    return tw.prep_activations(torch.from_numpy(np.ascontiguousarray(a)).cuda(), tw.Layout.ROW_MAJOR, dtype)
+
+
+def rel_l2(got, want):
+    return orc.rel_l2(got, want)
+
+
+@pytest.mark.parametrize("name", gio.small_names())
+def test_tw_gemm_matches_reference_golden(name):
+    c = gio.small_case(name)
+    p = to_tw_pattern(c["pattern"])
+    ts = tw.compact(tw.DenseMatrix.from_array(c["w"]), p)
+    plan = tw.TwPlan(ts)
+    at = device_at(c["a"])
+    ct = plan.gemm(at).cpu().numpy()
+    want = c["ct"]
+    assert ct.shape == want.shape
+    assert np.all(ct[c["pruned"]] == 0.0)  # pruned columns exactly zero
+    assert np.all(np.isfinite(ct))
+    assert rel_l2(ct, want) <= RTOL, rel_l2(ct, want)
+    # fp32 accumulation of exact bf16 products: far inside the bar
+    if np.abs(want).sum() > 0:
+        assert rel_l2(ct, want) < 1e-5
+
+
+@pytest.mark.parametrize("name", gio.small_names())
+def test_exact_kernel_bitexact_with_reference(name):
+    """CUDA-core kernel over the SAME packed plan, fp32 mul-then-add:
+    bit-identical to the reference's gemm_tw -- proves index lists, col ids,
+    zero rows and the swizzled weight image end to end."""
+    c = gio.small_case(name)
+    ts = tw.compact(tw.DenseMatrix.from_array(c["w"]), to_tw_pattern(c["pattern"]))
+    plan = tw.TwPlan(ts)
+    at32 = torch.from_numpy(np.ascontiguousarray(c["a"].T)).cuda()
+    ct = plan.gemm_exact(at32).cpu().numpy()
+    assert np.array_equal(ct, c["ct"])
+
+
+@pytest.mark.parametrize("name", [n for n in gio.small_names() if "csc" in gio.small_case(n)])
+def test_spmm_and_tew_vs_reference(name):
+    c = gio.small_case(name)
+    cp, ri, va = c["csc"]
+    csc = tw.CscMatrix(c["k"], c["n"], cp, ri, va)
+    dcsc = tw.DeviceCsc(csc)
+    # SpMM on fp32 activations: bit-exact (same rounding sequence)
+    at32 = torch.from_numpy(np.ascontiguousarray(c["a"].T)).cuda()
+    assert np.array_equal(tw.spmm_csc_device(at32, dcsc).cpu().numpy(), c["spmm_ct"])
+    # ... and on bf16 activations (bf16-representable inputs): still bit-exact
+    at = device_at(c["a"])
+    assert np.array_equal(tw.spmm_csc_device(at, dcsc).cpu().numpy(), c["spmm_ct"])
+    # TEW: TW (tensor cores) + SpMM into the same output
+    ts = tw.compact(tw.DenseMatrix.from_array(c["w"]), to_tw_pattern(c["pattern"]))
+    plan = tw.TwPlan(ts)
+    got = plan.gemm_tew(at, dcsc).cpu().numpy()
+    assert rel_l2(got, c["tew_ct"]) <= RTOL
+    assert rel_l2(got, c["tew_ct"]) < 1e-5
+
+
+def test_reference_signature_api_end_to_end():
+    """gemm_tw / gemm_tew / spmm_csc / gemm_dense with host DenseMatrix in
+    and COL_MAJOR DenseMatrix out, both input layouts."""
+    c = gio.small_case("g64_s60")
+    p = to_tw_pattern(c["pattern"])
+    w = tw.DenseMatrix.from_array(c["w"])
+    ts = tw.compact(w, p)
+    for layout in (tw.Layout.ROW_MAJOR, tw.Layout.COL_MAJOR):
+        a = tw.DenseMatrix.from_array(c["a"], layout)
+        out = tw.gemm_tw(a, ts, workers=4)
+        assert out.layout == tw.Layout.COL_MAJOR and out.shape == (c["m"], c["n"])
+        assert rel_l2(out.data.reshape(c["n"], c["m"]), c["ct"]) < 1e-5
+    cp, ri, va = c["csc"]
+    csc = tw.CscMatrix(c["k"], c["n"], cp, ri, va)
+    a = tw.DenseMatrix.from_array(c["a"])
+    assert np.array_equal(tw.spmm_csc(a, csc).data.reshape(c["n"], c["m"]), c["spmm_ct"])
+    assert rel_l2(tw.gemm_tew(a, ts, csc).data.reshape(c["n"], c["m"]), c["tew_ct"]) < 1e-5
+    dense = tw.gemm_dense(a, w).array()
+    want = (c["a"].astype(np.float64) @ c["w"].astype(np.float64))
+    assert rel_l2(dense, want) < 1e-5
+    with pytest.raises(tw.DimensionError):
+        tw.gemm_tw(tw.DenseMatrix.from_array(np.zeros((4, c["k"] + 1), np.float32)), ts)
+    with pytest.raises(tw.DimensionError):
+        tw.gemm_tw(a, ts, workers=0)
+
+
+def test_empty_overlay_is_exactly_gemm_tw():
+    c = gio.small_case("g16_s50")
+    ts = tw.compact(tw.DenseMatrix.from_array(c["w"]), to_tw_pattern(c["pattern"]))
+    a = tw.DenseMatrix.from_array(c["a"])
+    empty = tw.to_csc(tw.DenseMatrix.from_array(c["w"]), np.zeros((c["k"], c["n"]), bool))
+    assert np.array_equal(tw.gemm_tew(a, ts, empty).data, tw.gemm_tw(a, ts).data)
+
+
+def test_inf_in_pruned_rows_does_not_leak():
+    """The reference never multiplies pruned terms (0*inf would be NaN):
+    padding k indices must gather zeros, not real rows."""
+    c = gio.small_case("m_ragged")
+    p = to_tw_pattern(c["pattern"])
+    a = c["a"].copy()
+    never_kept = np.ones(c["k"], bool)
+    for t in p.tiles:
+        never_kept &= ~t.row_keep
+    if not never_kept.any():
+        pytest.skip("pattern keeps every row somewhere")
+    a[:, never_kept] = np.inf
+    ts = tw.compact(tw.DenseMatrix.from_array(c["w"]), p)
+    ct = tw.TwPlan(ts).gemm(device_at(a)).cpu().numpy()
+    assert np.all(np.isfinite(ct))
+    assert rel_l2(ct, c["ct"]) < 1e-5
+
+
+@pytest.mark.parametrize("out_dtype,bar", [(torch.float16, 1e-3), (torch.bfloat16, 5e-3)])
+def test_16bit_outputs(out_dtype, bar):
+    a, w, p = orc.bench_inputs(512, 768, 768, 128, 0.75, seed=11)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    plan = tw.TwPlan(ts)
+    at = device_at(a)
+    want = plan.gemm(at).cpu().numpy()
+    got = plan.gemm(at, out_dtype=out_dtype).float().cpu().numpy()
+    assert np.all(got[orc.pruned_columns(p)] == 0)
+    assert rel_l2(got, want) <= bar
+
+
+def test_fp16_operands():
+    a, w, p = orc.bench_inputs(300, 256, 384, 128, 0.5, seed=12, round_bf16=False)
+    a16, w16 = a.astype(np.float16).astype(np.float32), w.astype(np.float16).astype(np.float32)
+    ts = tw.compact(tw.DenseMatrix.from_array(w16), to_tw_pattern(p))
+    plan = tw.TwPlan(ts, dtype=torch.float16)
+    ct = plan.gemm(device_at(a16, torch.float16)).cpu().numpy()
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a16.T), orc.PackedTiles(orc.compact(w16, p), 256, 384))
+    assert rel_l2(ct, want) < 1e-5
+
+
+def test_accumulate_mode_adds_and_leaves_pruned_rows():
+    a, w, p = orc.bench_inputs(256, 128, 512, 128, 0.5, seed=13)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    plan = tw.TwPlan(ts)
+    at = device_at(a)
+    base = torch.full((512, 256), 2.0, device="cuda")
+    out = plan.gemm(at, out=base.clone(), accumulate=True).cpu().numpy()
+    ref = plan.gemm(at).cpu().numpy()
+    pr = orc.pruned_columns(p)
+    assert np.all(out[pr] == 2.0)
+    kept = np.setdiff1d(np.arange(512), pr)
+    assert np.allclose(out[kept], ref[kept] + 2.0, rtol=1e-6, atol=1e-5)
+
+
+@pytest.mark.parametrize("m", [1, 7, 64, 65, 129, 1000])
+def test_ragged_m(m):
+    a, w, p = orc.bench_inputs(m, 200, 300, 128, 0.6, seed=14)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    ct = tw.TwPlan(ts).gemm(device_at(a)).cpu().numpy()
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), 200, 300))
+    assert rel_l2(ct, want) < 1e-5
+    assert np.all(ct[orc.pruned_columns(p)] == 0)
+
+
+def test_strided_output_and_zero_m():
+    a, w, p = orc.bench_inputs(100, 128, 256, 64, 0.5, seed=15)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    plan = tw.TwPlan(ts)
+    at = device_at(a)
+    big = torch.full((256, 160), -7.0, device="cuda")
+    plan.gemm(at, out=big[:, :100])
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), 128, 256))
+    got = big.cpu().numpy()
+    assert rel_l2(got[:, :100], want) < 1e-5
+    assert np.all(got[:, 100:] == -7.0)
+    empty = torch.empty((128, 0), dtype=torch.bfloat16, device="cuda")
+    assert plan.gemm(empty).shape == (256, 0)
+
+
+def test_sharded_plans_reassemble_full_output():
+    a, w, p = orc.bench_inputs(384, 512, 1000, 128, 0.75, seed=16)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    at = device_at(a)
+    full = tw.TwPlan(ts).gemm(at).cpu().numpy()
+    parts = []
+    for c0, c1 in [(0, 250), (250, 500), (500, 750), (750, 1000)]:
+        parts.append(tw.TwPlan(ts, col_range=(c0, c1)).gemm(at).cpu().numpy())
+    assert np.array_equal(np.concatenate(parts), full)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2b", "C2a"])
+def test_full_size_vs_oracle(name):
+    """BASELINE shapes at full size vs the C oracle (itself pinned to the
+    reference by SHA-256, tests/test_oracle.py)."""
+    h = gio.load("golden_hashes.json")[name]
+    m, k, n, g, s = h["dims"]
+    a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
+    at32 = np.ascontiguousarray(a.T)
+    want = orc.gemm_tw_ct(at32, orc.PackedTiles(orc.compact(w, p), k, n), threads=orc.max_threads())
+    assert hashlib.sha256(want.tobytes()).hexdigest() == h["gemm_tw_sha256"]
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    plan = tw.TwPlan(ts)
+    ct = plan.gemm(device_at(a)).cpu().numpy()
+    assert rel_l2(ct, want) < 1e-5
+    assert np.all(ct[orc.pruned_columns(p)] == 0)
+    # exact CUDA-core path reproduces the reference bit for bit at full size
+    ex = plan.gemm_exact(torch.from_numpy(at32).cuda()).cpu().numpy()
+    assert hashlib.sha256(ex.tobytes()).hexdigest() == h["gemm_tw_sha256"]
+
+
+def test_tew_full_size_c4():
+    h = gio.load("golden_hashes.json")["C4"]
+    m, k, n, g, s = h["dims"]
+    a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
+    cp, ri, va = orc.tew_overlay_magnitude(w, p, h["delta"])
+    assert int(cp[-1]) == h["nnz"]
+    want = orc.gemm_tew_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), k, n), cp, ri, va,
+                           threads=orc.max_threads())
+    assert hashlib.sha256(want.tobytes()).hexdigest() == h["gemm_tew_sha256"]
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    got = tw.TwPlan(ts).gemm_tew(device_at(a), tw.DeviceCsc(tw.CscMatrix(k, n, cp, ri, va))).cpu().numpy()
+    assert rel_l2(got, want) < 1e-5
+
+
+def test_large_g256_and_bertlarge_shape():
+    a, w, p = orc.bench_inputs(2048, 1024, 4096, 256, 0.5, seed=17)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    ct = tw.TwPlan(ts).gemm(device_at(a)).cpu().numpy()
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), 1024, 4096),
+                          threads=orc.max_threads())
+    assert rel_l2(ct, want) < 1e-5
+
+
+def test_concurrent_streams_same_plan():
+    a, w, p = orc.bench_inputs(1024, 768, 768, 128, 0.75, seed=18)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    plan = tw.TwPlan(ts)
+    at = device_at(a)
+    ref = plan.gemm(at)
+    outs = []
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    torch.cuda.synchronize()
+    for s in streams:
+        with torch.cuda.stream(s):
+            outs.append(plan.gemm(at, stream=s))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
