@@ -225,7 +225,7 @@ class DeviceCsc:
         self.rows, self.cols, self.nnz = s.rows, s.cols, s.nnz
         self.col_ptr = torch.from_numpy(np.asarray(s.col_ptr, np.int64).astype(np.int32)).to(dev)
         self.row_idx = torch.from_numpy(np.asarray(s.row_idx, np.int64).astype(np.int32).reshape(-1)).to(dev)
-        self.values = torch.from_numpy(np.ascontiguousarray(s.values, np.float32).reshape(-1)).to(dev)
+        self.values = torch.from_numpy(np.array(s.values, np.float32).reshape(-1)).to(dev)
         if self.nnz == 0:  # keep valid pointers
             self.row_idx = torch.zeros(1, dtype=torch.int32, device=dev)
             self.values = torch.zeros(1, dtype=torch.float32, device=dev)
