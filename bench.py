@@ -1,0 +1,446 @@
+"""Benchmark: TW-sparse GEMM on B200 vs dense cuBLAS bf16 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--out-dtype fp32|fp16|bf16] [--workload C2a|C2b|C1|C5_75|C4]
+
+One step = one pass of the hot path over one batch: gemm_tw of the BERT-base
+FC1 layer (M=4096 tokens, K=768, N=3072, G=128, 75% TW sparsity, pattern
+random_uniform_pattern(seed 42), A/W ~ N(0,1) from default_rng(42) rounded
+to bf16 -- the reference's own bench recipe, cli.py:408-412).  Inputs are
+resident in HBM for `value` (A^T bf16, packed plan); `e2e` runs the
+reference-signature API with host fp32 buffers in pinned memory (H2D +
+transpose/cast + GEMM + D2H of the fp32 C inside the timed region).
+
+Multi-GPU (torchrun, one rank per GPU): the layer's N dimension is sharded
+(column tiles), each rank computes its own N=3072 slice of an N=3072*P layer
+(weak scaling, no data-path collective in the timed region); the NCCL
+all-gather that reassembles C^T is timed separately and reported.
+
+--impl reference: the reference's CPU algorithm (the C port in oracle/,
+test infrastructure -- the reference itself is Python+numba and does not
+travel to the GPU box) on the host cores, same metric/config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TW-GEMM effective TFLOPS & speedup vs dense cuBLAS bf16 at 75% sparsity"
+UNIT = "TFLOPS (dense-equivalent 2*M*K*N / t)"
+WORKLOADS = {
+    # name: (M, K, N, G, s, description)
+    "C2a": (4096, 768, 3072, 128, 0.75, "BERT-base FC1 M=4096 K=768 N=3072, G=128, 75% TW"),
+    "C2b": (4096, 768, 768, 128, 0.75, "BERT-base attn-out M=4096 K=768 N=768, G=128, 75% TW"),
+    "C1": (1024, 1024, 1024, 128, 0.50, "M=N=K=1024, G=128, 50% TW"),
+    "C5_75": (16384, 1024, 4096, 128, 0.75, "BERT-large FC1 M=16384 K=1024 N=4096, G=128, 75% TW"),
+}
+L2_BYTES = 126 * 2**20
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clocks + throttle reasons via NVML while running."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append(mhz)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=1)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def to_pattern(tw, p):
+    k, n, g, tiles = p
+    return tw.TilePattern(k, n, g, tuple(tw.Tile(c, keep) for c, keep in tiles))
+
+
+def algorithmic_bytes(info, m: int, out_bytes: int) -> int:
+    """A read once (union of kept rows), W once, dense C (incl.
+    zero columns), int32 index lists."""
+    n_rows = info["col_end"] - info["col_begin"]
+    return (2 * m * info["union_k"] + 2 * info["kept_elems"] + out_bytes * m * n_rows
+            + 4 * (info["sum_k"] + info["sum_n"]))
+
+
+def time_device(torch, fn, steps: int, warmup: int, soak_s: float = 0.0, graph: bool = True):
+    """Warm up (eager), capture the `steps` launches into one CUDA graph
+    (removes per-launch host overhead; every kernel still runs), optionally
+    soak (untimed) so clocks settle, then time one replay of exactly `steps`
+    steps with CUDA events on the launching stream.  Returns ms per step."""
+    for i in range(warmup):
+        fn(i)
+    torch.cuda.synchronize()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(steps):
+                fn(i)
+        torch.cuda.synchronize()
+        run = g.replay
+    else:
+        def run():
+            for i in range(steps):
+                fn(i)
+    if soak_s > 0:
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < soak_s:
+            run()
+            torch.cuda.synchronize()
+    else:
+        run()
+        torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    run()
+    end.record(stream)
+    torch.cuda.synchronize()
+    return start.elapsed_time(end) / steps
+
+
+def read_traffic(workload: str, out_dtype: str):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d.get(f"{workload}:{out_dtype}")
+
+
+# ---------------------------------------------------------------- CPU arm
+def cpu_reference_time(orc, a, w, p, m_sample: int, threads: int, repeats: int):
+    """Times the reference's CPU algorithm (oracle C port of gemm_tw,
+    engine.py:126-164 / _kernels.py:13-27) on an M-row sample."""
+    k, n = p[0], p[1]
+    packed = orc.PackedTiles(orc.compact(w, p), k, n)
+    at = np.ascontiguousarray(a[:m_sample].T)
+    out = np.empty((n, m_sample), np.float32)
+    orc.gemm_tw_ct(at, packed, threads=threads, out=out)  # warm-up (time_median semantics)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        orc.gemm_tw_ct(at, packed, threads=threads, out=out)
+        times.append(time.perf_counter() - t0)
+    return statistics.median(times)
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    m, k, n, g, s, desc = WORKLOADS[args.workload]
+    a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
+    threads = orc.max_threads()
+    dense_flops = 2 * m * k * n
+    # size the per-step sample so the whole run stays within ~2 minutes
+    probe_m = min(m, 512)
+    t_probe = cpu_reference_time(orc, a, w, p, probe_m, threads, 1)
+    est_full = t_probe * m / probe_m
+    total_steps = args.steps + args.warmup
+    m_sample = m if est_full * total_steps <= 120 else max(128, int(120 / total_steps / t_probe * probe_m) // 128 * 128)
+    m_sample = min(m_sample, m)
+    packed = orc.PackedTiles(orc.compact(w, p), k, n)
+    at = np.ascontiguousarray(a[:m_sample].T)
+    out = np.empty((n, m_sample), np.float32)
+    for _ in range(args.warmup):
+        orc.gemm_tw_ct(at, packed, threads=threads, out=out)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.gemm_tw_ct(at, packed, threads=threads, out=out)
+        times.append(time.perf_counter() - t0)
+    t_full = statistics.median(times) * m / m_sample
+    value = dense_flops / t_full / 1e12
+    sample = (f"{'full workload' if m_sample == m else f'{m_sample} of {m} token rows (scaled to M)'}; "
+              f"median of {args.steps} steps after {args.warmup} warm-up")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": desc, "m": m, "k": k, "n": n, "g": g, "sparsity": s},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("reference CPU algorithm = oracle/tw_oracle.c, a bit-exact C port of tilewise's numba "
+                 "mm_accum/gemm_tw (pinned by SHA-256 against the reference's outputs); parallel over tiles "
+                 "(disjoint output rows), i.e. at least as fast as the reference's group-level pool"),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+
+    import paper_2008_13006_b200 as tw
+    from oracle import oracle as orc  # checker + cpu_baseline only
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    m, k, n_layer, g, s, desc = WORKLOADS[args.workload]
+    hbm_peak, tc_peak, peak_kind = load_peaks()
+    out_dt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[args.out_dtype]
+    out_bytes = 4 if args.out_dtype == "fp32" else 2
+
+    # weak scaling: an N = n_layer * world layer, rank r owns columns [r*n_layer, (r+1)*n_layer)
+    n_total = n_layer * world
+    a, w, p = orc.bench_inputs(m, k, n_total, g, s, seed=42)
+    pat = to_pattern(tw, p)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), pat)
+    col_range = (rank * n_layer, (rank + 1) * n_layer)
+    plan = tw.TwPlan(ts, device=dev, col_range=col_range)
+    info = plan.info
+    dense_flops = 2 * m * k * n_layer
+    kept_flops = plan.kept_flops(m)
+
+    # rotating buffer sets so consecutive steps never hit in L2
+    at0 = tw.prep_activations(torch.from_numpy(a).to(dev), tw.Layout.ROW_MAJOR, torch.bfloat16)
+    set_bytes = 2 * k * m + out_bytes * n_layer * m + info["wimg_bytes"]
+    n_sets = max(2, int(np.ceil(2 * L2_BYTES / set_bytes)) + 1)
+    ats = [at0] + [at0.clone() for _ in range(n_sets - 1)]
+    plans = [plan] + [tw.TwPlan(ts, device=dev, col_range=col_range) for _ in range(n_sets - 1)]
+    outs = [torch.empty((n_layer, m), dtype=out_dt, device=dev) for _ in range(n_sets)]
+
+    # parity gate (untimed): GPU result vs the CPU oracle on this rank's slice
+    ct = plan.gemm(at0, out_dtype=torch.float32).cpu().numpy()
+    sub = orc.compact(w, p)
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(sub, k, n_total),
+                          threads=orc.max_threads())[col_range[0]:col_range[1]]
+    parity = orc.rel_l2(ct, want)
+    zeros_ok = bool(np.all(ct[orc.pruned_columns(p)[(orc.pruned_columns(p) >= col_range[0]) &
+                                                   (orc.pruned_columns(p) < col_range[1])] - col_range[0]] == 0))
+    del ct, want
+
+    def step(i):
+        j = i % n_sets
+        plans[j].gemm(ats[j], out=outs[j], out_dtype=out_dt)
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region (device events), clocks sampled during soak + timing
+    barrier()
+    with ClockSampler(local) as clk:
+        ms = time_device(torch, step, args.steps, args.warmup, soak_s=args.soak)
+    barrier()
+    ms_all = ms
+    if pg is not None:
+        t = torch.tensor([ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms_all = float(t.item())
+    value = world * dense_flops / (ms_all * 1e-3) / 1e12
+
+    # ---- dominant kernel roofline: the TW kernel is the only launch per step
+    bytes_alg = algorithmic_bytes(info, m, out_bytes)
+    achieved = bytes_alg / (ms * 1e-3) / 1e9
+    traffic = read_traffic(args.workload, args.out_dtype)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "tw_gemm_sm100_kernel", "algorithmic_bytes_per_launch": bytes_alg,
+                "kept_tflops": kept_flops / (ms * 1e-3) / 1e12,
+                "tensor_frac_of_bf16_peak": kept_flops / (ms * 1e-3) / 1e12 / tc_peak}
+
+    result = {}
+    if rank == 0:
+        # same steps launched eagerly from Python (per-call host overhead visible)
+        result["eager_ms"] = time_device(torch, step, args.steps, 3, graph=False)
+        # ---- other output dtypes (same kernel, 16-bit epilogue)
+        variants = {}
+        for name, dt, ob in (("fp16_out", torch.float16, 2), ("bf16_out", torch.bfloat16, 2), ("fp32_out", torch.float32, 4)):
+            if dt == out_dt:
+                continue
+            vo = [torch.empty((n_layer, m), dtype=dt, device=dev) for _ in range(n_sets)]
+            vms = time_device(torch, lambda i: plans[i % n_sets].gemm(ats[i % n_sets], out=vo[i % n_sets], out_dtype=dt),
+                              args.steps, args.warmup)
+            b = algorithmic_bytes(info, m, ob)
+            variants[name] = {"ms_per_step": vms, "tflops_dense_equiv": dense_flops / (vms * 1e-3) / 1e12,
+                              "hbm_gbs": b / (vms * 1e-3) / 1e9, "hbm_frac": b / (vms * 1e-3) / 1e9 / hbm_peak}
+            del vo
+        # ---- dense cuBLAS bf16 baseline at the same shape (rotating buffers)
+        a_bf = torch.from_numpy(a).to(dev, torch.bfloat16)
+        w_bf = torch.from_numpy(w[:, col_range[0]:col_range[1]].copy()).to(dev, torch.bfloat16)
+        a_sets = [a_bf] + [a_bf.clone() for _ in range(n_sets - 1)]
+        w_sets = [w_bf] + [w_bf.clone() for _ in range(n_sets - 1)]
+        c16 = [torch.empty((m, n_layer), dtype=torch.bfloat16, device=dev) for _ in range(n_sets)]
+        cub16 = time_device(torch, lambda i: torch.mm(a_sets[i % n_sets], w_sets[i % n_sets], out=c16[i % n_sets]),
+                            args.steps, args.warmup)
+        del c16
+        c32 = [torch.empty((m, n_layer), dtype=torch.float32, device=dev) for _ in range(n_sets)]
+        cub32 = time_device(torch, lambda i: torch.mm(a_sets[i % n_sets], w_sets[i % n_sets], out_dtype=torch.float32,
+                                                      out=c32[i % n_sets]), args.steps, args.warmup)
+        del c32, a_sets, w_sets
+        result.update(cublas={"bf16_out_ms": cub16, "fp32_out_ms": cub32,
+                              "bf16_out_tflops": dense_flops / (cub16 * 1e-3) / 1e12,
+                              "fp32_out_tflops": dense_flops / (cub32 * 1e-3) / 1e12},
+                      variants=variants)
+
+        # ---- e2e through the reference-signature API with host buffers
+        import torch as _t
+        a_pin = _t.empty(m * k, dtype=_t.float32, pin_memory=True)
+        a_pin.copy_(_t.from_numpy(a.reshape(-1)))
+        a_host = tw.DenseMatrix(m, k, tw.Layout.ROW_MAJOR, a_pin.numpy())
+        c_pin = _t.empty(m * n_total, dtype=_t.float32, pin_memory=True).numpy()
+        e2e_ts = ts if world == 1 else None
+        if e2e_ts is not None:
+            for _ in range(max(2, args.warmup)):
+                tw.gemm_tw(a_host, e2e_ts, out=c_pin)
+            e_steps = max(3, min(args.steps, 50))
+            t0 = time.perf_counter()
+            for _ in range(e_steps):
+                r = tw.gemm_tw(a_host, e2e_ts, out=c_pin)
+            e2e_s = (time.perf_counter() - t0) / e_steps
+            assert r.shape == (m, n_total)
+            result["e2e"] = {"value": dense_flops / e2e_s / 1e12, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+                             "h2d_bytes_per_step": 4 * m * k, "d2h_bytes_per_step": 4 * m * n_total,
+                             "api": "paper_2008_13006_b200.gemm_tw(DenseMatrix fp32 host, CompactTileSet) -> "
+                                    "COL_MAJOR DenseMatrix (pinned host buffers)"}
+
+        # ---- CPU baseline: reference algorithm (oracle C port) on host cores
+        if world == 1 and not args.no_cpu:
+            threads = orc.max_threads()
+            m_s = min(m, args.cpu_sample_m)
+            t_cpu = cpu_reference_time(orc, a, w, p, m_s, threads, repeats=3) * m / m_s
+            result["cpu_baseline"] = {"value": dense_flops / t_cpu / 1e12, "unit": UNIT, "cores": threads,
+                                      "kind": "port",
+                                      "sample": f"gemm_tw on {m_s} of {m} token rows, median of 3 after 1 warm-up, "
+                                                f"scaled to M; oracle/tw_oracle.c (bit-exact C port of the reference)",
+                                      "ms_per_step": t_cpu * 1e3}
+
+    # ---- multi-GPU: NCCL all-gather that reassembles C^T (not in `value`)
+    if pg is not None:
+        full = torch.empty((n_total, m), dtype=out_dt, device=dev)
+        def ag(i):
+            pg.all_gather_into_tensor(full, outs[i % n_sets])
+        barrier()
+        ag_ms = time_device(torch, ag, max(3, args.steps // 4), 2, graph=False)
+        t = torch.tensor([ag_ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        result["allgather"] = {"ms": float(t.item()), "bytes_per_rank_in": (world - 1) * out_bytes * n_layer * m,
+                               "note": "ncclAllGather of C^T row blocks over NVLink; reported, not in value"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_all, "ms_per_step_eager_launch": result.get("eager_ms"),
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": desc, "m": m, "k": k, "n_per_gpu": n_layer, "g": g, "sparsity": s,
+                       "element_sparsity": 1 - info["kept_elems"] / (k * n_layer), "out_dtype": args.out_dtype,
+                       "inputs": "A^T bf16 + packed plan resident in HBM",
+                       "l2": f"{n_sets} rotating input/output/plan sets ({n_sets * set_bytes / 2**20:.0f} MB) > 2x L2",
+                       "parallelism": f"N-sharded x{world}" if world > 1 else "single GPU"},
+            "kept_tflops": kept_flops / (ms * 1e-3) / 1e12,
+            "speedup_vs_cublas_bf16": result["cublas"]["bf16_out_ms"] / ms,
+            "speedup_vs_cublas_bf16_same_out_dtype": (result["cublas"]["fp32_out_ms"] if args.out_dtype == "fp32"
+                                                      else result["cublas"]["bf16_out_ms"]) / ms,
+            "cublas": result["cublas"], "variants": result["variants"],
+            "parity": {"rel_l2_vs_oracle": parity, "pruned_cols_exact_zero": zeros_ok, "bar": 1e-3},
+            "roofline": roofline, "cpu_baseline": result.get("cpu_baseline"), "e2e": result.get("e2e"),
+            "gpu_launches": args.steps, "clocks": clk.summary(),
+        }
+        if "allgather" in result:
+            line["allgather"] = result["allgather"]
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2a", choices=sorted(WORKLOADS))
+    ap.add_argument("--out-dtype", default="fp32", choices=["fp32", "fp16", "bf16"])
+    ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds before timing (clock settle)")
+    ap.add_argument("--cpu-sample-m", type=int, default=4096)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -293,18 +293,32 @@ def _as_tileset(tiles) -> CompactTileSet:
 
 
 def _device_activations(a: DenseMatrix, device, dtype):
-    """Host DenseMatrix -> device A^T (K x M) in `dtype` via pinned memory."""
-    host = torch.from_numpy(np.asarray(a.data, np.float32)).pin_memory()
-    dev = host.to(device, non_blocking=True)
+    """Host DenseMatrix -> device A^T (K x M) in `dtype`.  The fp32 buffer is
+    copied as-is (asynchronously when it lives in pinned memory) and
+    transposed / cast on the device by the prep kernel."""
+    data = np.asarray(a.data, np.float32)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # frozen (read-only) buffers are only read here
+        host = torch.from_numpy(data)
+    dev = host.to(device, non_blocking=host.is_pinned())
     if a.layout == Layout.ROW_MAJOR:
         return prep_activations(dev.view(a.rows, a.cols), Layout.ROW_MAJOR, dtype)
     return prep_activations(dev.view(a.cols, a.rows), Layout.COL_MAJOR, dtype)
 
 
-def _to_host_colmajor(ct, rows: int, cols: int) -> DenseMatrix:
-    host = torch.empty(ct.shape, dtype=ct.dtype, pin_memory=True)
-    host.copy_(ct, non_blocking=False)
-    return DenseMatrix(rows, cols, Layout.COL_MAJOR, host.numpy().astype(np.float32, copy=False).reshape(-1).copy())
+def _to_host_colmajor(ct, rows: int, cols: int, out=None) -> DenseMatrix:
+    """Device C^T -> COL_MAJOR DenseMatrix.  `out` (a float32 numpy array of
+    rows*cols elements, ideally in pinned memory) receives the buffer; the
+    returned matrix views it."""
+    if out is None:
+        buf = np.empty(rows * cols, np.float32)
+    else:
+        buf = np.asarray(out).reshape(-1)
+        if buf.dtype != np.float32 or buf.size != rows * cols:
+            raise DimensionError(f"out must hold {rows * cols} float32 values")
+    torch.from_numpy(buf).view(ct.shape).copy_(ct)
+    return DenseMatrix(rows, cols, Layout.COL_MAJOR, buf)
 
 
 def _check_workers(workers: int) -> None:
@@ -312,10 +326,11 @@ def _check_workers(workers: int) -> None:
         raise DimensionError(f"workers must be >= 1, got {workers}")  # engine.py:97-98
 
 
-def gemm_tw(a: DenseMatrix, tiles: CompactTileSet, workers: int = 1, *, device=None) -> DenseMatrix:
+def gemm_tw(a: DenseMatrix, tiles: CompactTileSet, workers: int = 1, *, device=None, out=None) -> DenseMatrix:
     """engine.py:152-164: C = A x expand(tiles) as a COL_MAJOR DenseMatrix.
     Pruned columns are exactly zero.  Computes on the GPU with bf16 operands
-    and fp32 accumulation/output."""
+    and fp32 accumulation/output.  `out`: optional float32 host array
+    (M*N, pinned for full copy bandwidth) that receives the C^T buffer."""
     a = as_dense(a)
     tiles = _as_tileset(tiles)
     if a.cols != tiles.k:
@@ -327,10 +342,20 @@ def gemm_tw(a: DenseMatrix, tiles: CompactTileSet, workers: int = 1, *, device=N
     plan = _plan_for(tiles, device)
     at = _device_activations(a, device, plan.dtype)
     ct = plan.gemm(at, out_dtype=torch.float32)
-    return _to_host_colmajor(ct, a.rows, tiles.n)
+    return _to_host_colmajor(ct, a.rows, tiles.n, out)
 
 
-def spmm_csc(a: DenseMatrix, s: CscMatrix, *, device=None) -> DenseMatrix:
+def _device_csc(s: CscMatrix, device) -> DeviceCsc:
+    cache = getattr(s, "_tw_b200_dev", None)
+    if cache is None:
+        cache = {}
+        object.__setattr__(s, "_tw_b200_dev", cache)
+    if str(device) not in cache:
+        cache[str(device)] = DeviceCsc(s, device)
+    return cache[str(device)]
+
+
+def spmm_csc(a: DenseMatrix, s: CscMatrix, *, device=None, out=None) -> DenseMatrix:
     """engine.py:167-181 on the GPU (fp32 activations: bit-exact)."""
     a, s = as_dense(a), as_csc(s)
     if a.cols != s.rows:
@@ -339,11 +364,12 @@ def spmm_csc(a: DenseMatrix, s: CscMatrix, *, device=None) -> DenseMatrix:
     if a.rows == 0:
         return DenseMatrix(0, s.cols, Layout.COL_MAJOR, np.zeros(0, np.float32))
     at = _device_activations(a, device, torch.float32)
-    ct = spmm_csc_device(at, DeviceCsc(s, device))
-    return _to_host_colmajor(ct, a.rows, s.cols)
+    ct = spmm_csc_device(at, _device_csc(s, device))
+    return _to_host_colmajor(ct, a.rows, s.cols, out)
 
 
-def gemm_tew(a: DenseMatrix, tiles: CompactTileSet, ew: CscMatrix, workers: int = 1, *, device=None) -> DenseMatrix:
+def gemm_tew(a: DenseMatrix, tiles: CompactTileSet, ew: CscMatrix, workers: int = 1, *, device=None,
+             out=None) -> DenseMatrix:
     """engine.py:184-198: gemm_tw + spmm_csc over all N columns."""
     a, ew = as_dense(a), as_csc(ew)
     tiles = _as_tileset(tiles)
@@ -353,14 +379,14 @@ def gemm_tew(a: DenseMatrix, tiles: CompactTileSet, ew: CscMatrix, workers: int 
         raise DimensionError(f"A has {a.cols} cols but pattern K is {tiles.k}")
     _check_workers(workers)
     if ew.nnz == 0:
-        return gemm_tw(a, tiles, workers, device=device)
+        return gemm_tw(a, tiles, workers, device=device, out=out)
     device = device or torch.device("cuda", torch.cuda.current_device())
     if a.rows == 0:
         return DenseMatrix(0, tiles.n, Layout.COL_MAJOR, np.zeros(0, np.float32))
     plan = _plan_for(tiles, device)
     at = _device_activations(a, device, plan.dtype)
-    ct = plan.gemm_tew(at, DeviceCsc(ew, device), out_dtype=torch.float32)
-    return _to_host_colmajor(ct, a.rows, tiles.n)
+    ct = plan.gemm_tew(at, _device_csc(ew, device), out_dtype=torch.float32)
+    return _to_host_colmajor(ct, a.rows, tiles.n, out)
 
 
 def gemm_dense(a: DenseMatrix, b: DenseMatrix, *, device=None) -> DenseMatrix:
