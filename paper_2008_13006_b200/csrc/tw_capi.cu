@@ -210,6 +210,7 @@ int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, 
   const uint32_t ab = hp.in_dtype == TW_BF16 ? 1u : 0u;
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 15) | ((128u >> 4) << 24);
   a.block_n = hp.block_n;
+  a.avg_cols = n_live > 0 ? (int32_t)(hp.sum_n / n_live) : 0;
   const int64_t units = n_live * a.mblocks;
   const int64_t zero_bytes = (int64_t)a.n_zero * m * out_size(out_dtype);
   int64_t grid = units;

@@ -70,23 +70,50 @@ __device__ __forceinline__ float cvt_in<__nv_bfloat16>(__nv_bfloat16 v) { return
 template <>
 __device__ __forceinline__ float cvt_in<__half>(__half v) { return __half2float(v); }
 
-// zero rows [r0, r1) of the zero list, full M, by the 128 epilogue threads
-template <typename OutT>
-__device__ __forceinline__ void write_zero_rows(const GemmArgs &a, int r0, int r1, int et) {
-  const int64_t row_bytes = (int64_t)a.M * sizeof(OutT);
-  const bool vec = ((a.ldc * (int64_t)sizeof(OutT)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
-  for (int r = r0; r < r1; ++r) {
-    const int row = __ldg(a.zero_rows + r);
-    char *base = reinterpret_cast<char *>(a.out) + (int64_t)row * a.ldc * sizeof(OutT);
-    if (vec) {
-      const int64_t n16 = row_bytes / 16;
-      uint4 z = make_uint4(0, 0, 0, 0);
-      for (int64_t i = et; i < n16; i += 128) reinterpret_cast<uint4 *>(base)[i] = z;
-      for (int64_t i = n16 * 16 / sizeof(OutT) + et; i < a.M; i += 128) reinterpret_cast<OutT *>(base)[i] = cvt_out<OutT>(0.f);
-    } else {
-      for (int64_t i = et; i < a.M; i += 128) reinterpret_cast<OutT *>(base)[i] = cvt_out<OutT>(0.f);
-    }
+// streaming (evict-first) store of one output element
+template <typename T>
+__device__ __forceinline__ void st_cs(T *p, T v) {
+  if constexpr (sizeof(T) == 4) {
+    __stcs(reinterpret_cast<float *>(p), *reinterpret_cast<float *>(&v));
+  } else {
+    __stcs(reinterpret_cast<unsigned short *>(p), *reinterpret_cast<unsigned short *>(&v));
   }
+}
+
+// Zero rows [r0, r1) of the zero list (pruned columns of C), full M.  Called
+// by the 4 epilogue warps; warp ew writes rows r0+ew, r0+ew+4, ... with
+// coalesced 16-byte streaming stores (512 B per warp instruction).  The next
+// row id is prefetched so the index load latency is paid once.
+template <typename OutT>
+__device__ __forceinline__ void write_zero_rows(const GemmArgs &a, int r0, int r1, int ew, int lane) {
+  const bool vec = ((a.ldc * (int64_t)sizeof(OutT)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
+  const int64_t n16 = vec ? (int64_t)a.M * (int64_t)sizeof(OutT) / 16 : 0;
+  const int64_t tail0 = n16 * 16 / (int64_t)sizeof(OutT);
+  int r = r0 + ew;
+  int row = r < r1 ? __ldg(a.zero_rows + r) : 0;
+  for (; r < r1; r += 4) {
+    const int next = (r + 4 < r1) ? __ldg(a.zero_rows + r + 4) : 0;
+    OutT *base = reinterpret_cast<OutT *>(a.out) + (int64_t)row * a.ldc;
+    uint4 *b16 = reinterpret_cast<uint4 *>(base);
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int64_t i = lane; i < n16; i += 32) __stcs(b16 + i, z);
+    for (int64_t i = tail0 + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(0.f);
+    row = next;
+  }
+}
+
+// First zero-list row owned by CTA c: zero rows are dealt out so that every
+// CTA writes about the same number of output bytes (its MMA units' columns
+// plus its zero rows), i.e. CTAs with one unit fewer take more zero rows.
+__device__ __forceinline__ int zero_split(const GemmArgs &a, int c, int G, int units, int64_t unit_bytes,
+                                          int64_t row_bytes) {
+  if (c >= G) return a.n_zero;
+  const int64_t q = units / G, rem = units % G;
+  const int64_t before = (int64_t)c * q + min((int64_t)c, rem);
+  const int64_t total = (int64_t)units * unit_bytes + (int64_t)a.n_zero * row_bytes;
+  const int64_t want = total / G * c - before * unit_bytes;
+  int64_t z = want <= 0 ? 0 : want / row_bytes;
+  return (int)min(z, (int64_t)a.n_zero);
 }
 
 template <int BN, typename OutT>
@@ -126,30 +153,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint64_t keep = ptx::policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-        const TileMeta t = args.tiles[u / args.mblocks];
-        const int m0 = (u % args.mblocks) * kBlockM;
-        const int4 *ki = reinterpret_cast<const int4 *>(args.kidx + t.kidx_off);
-        const uint8_t *wsrc = args.wimg + t.w_off;
-        for (int kb = 0; kb < t.nkb; ++kb) {
+    // ------------------------------------------------ TMA producer (whole warp)
+    // Lane l < 16 owns kept-k rows 4l..4l+3 of each 64-row stage: it loads
+    // their indices one stage ahead (one coalesced 256 B load per stage) and
+    // issues the two gather4 copies (token halves) for them; lane 0 handles
+    // the barriers and the weight-image bulk copy.
+    const uint64_t keep = ptx::policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      const TileMeta t = args.tiles[u / args.mblocks];
+      const int m0 = (u % args.mblocks) * kBlockM;
+      const int4 *ki = reinterpret_cast<const int4 *>(args.kidx + t.kidx_off);
+      const uint8_t *wsrc = args.wimg + t.w_off;
+      int4 rows_next = lane < 16 ? __ldg(ki + lane) : make_int4(0, 0, 0, 0);
+      for (int kb = 0; kb < t.nkb; ++kb) {
+        const int4 rows = rows_next;
+        if (kb + 1 < t.nkb && lane < 16) rows_next = __ldg(ki + (kb + 1) * 16 + lane);
+        if (lane == 0) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], kABytes + (uint32_t)args.wbytes);
           ptx::bulk_g2s(sB + stage * C::kBBytes, wsrc + (int64_t)kb * args.wbytes, (uint32_t)args.wbytes,
                         &full[stage], keep);
-          uint8_t *a_dst = sA + stage * kABytes;
-#pragma unroll 4
-          for (int g = 0; g < kBlockK / 4; ++g) {
-            const int4 rows = __ldg(ki + kb * (kBlockK / 4) + g);
-            ptx::tma_gather4(a_dst + g * 512, &tmap_at, &full[stage], m0, rows, keep);
-            ptx::tma_gather4(a_dst + 8192 + g * 512, &tmap_at, &full[stage], m0 + 64, rows, keep);
-          }
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (lane < 16) {
+          uint8_t *a_dst = sA + stage * kABytes + lane * 512;
+          ptx::tma_gather4(a_dst, &tmap_at, &full[stage], m0, rows, keep);
+          ptx::tma_gather4(a_dst + 8192, &tmap_at, &full[stage], m0 + 64, rows, keep);
+        }
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -189,40 +222,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------ epilogue (128 threads)
-    const int et = threadIdx.x - 64;   // 0..127
-    const int q = warp & 3;            // TMEM lane quadrant this warp may access
-    // this CTA's share of the zero rows, interleaved with its MMA units
+    const int q = warp & 3;   // TMEM lane quadrant this warp may access
+    const int ew = warp - 2;  // 0..3
+    const int G = gridDim.x;
+    const int64_t row_bytes = (int64_t)args.M * sizeof(OutT);
+    const int64_t unit_bytes = (int64_t)kBlockM * args.avg_cols * sizeof(OutT);
     int z0 = 0, z1 = 0;
     if (!args.accumulate && args.n_zero > 0) {
-      z0 = (int)((int64_t)args.n_zero * blockIdx.x / gridDim.x);
-      z1 = (int)((int64_t)args.n_zero * (blockIdx.x + 1) / gridDim.x);
+      z0 = zero_split(args, blockIdx.x, G, total_units, unit_bytes, row_bytes);
+      z1 = max(z0, zero_split(args, blockIdx.x + 1, G, total_units, unit_bytes, row_bytes));
     }
-    const int my_units = blockIdx.x < total_units ? (total_units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int my_units = blockIdx.x < total_units ? (total_units - 1 - blockIdx.x) / G + 1 : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int i = 0;
     OutT *out = reinterpret_cast<OutT *>(args.out);
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++i) {
-      // zero part i of my_units (written while unit i's mainloop runs)
-      write_zero_rows<OutT>(args, z0 + (z1 - z0) * i / my_units, z0 + (z1 - z0) * (i + 1) / my_units, et);
+    for (int u = blockIdx.x; u < total_units; u += G, ++i) {
       const TileMeta t = args.tiles[u / args.mblocks];
+      int cid[BN / 32];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c)
+        cid[c] = (c * 32 + lane < t.n_i) ? __ldg(args.colids + t.col_off + c * 32 + lane) : -1;
+      // zero part i of my_units (written while unit i's mainloop runs)
+      write_zero_rows<OutT>(args, z0 + (z1 - z0) * i / my_units, z0 + (z1 - z0) * (i + 1) / my_units, ew, lane);
       const int m = (u % args.mblocks) * kBlockM + q * 32 + lane;
+      const bool m_ok = m < args.M;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-      for (int c0 = 0; c0 < t.n_i; c0 += 32) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(t_row + (uint32_t)c0, v);
-        const int cid = (c0 + lane < t.n_i) ? __ldg(args.colids + t.col_off + c0 + lane) : -1;
-        ptx::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int row = __shfl_sync(0xffffffffu, cid, j);
-          if (row >= 0 && m < args.M) {
-            OutT *p = out + (int64_t)row * args.ldc + m;
-            float val = __uint_as_float(v[j]);
-            if (args.accumulate) val += cvt_in<OutT>(*p);
-            *p = cvt_out<OutT>(val);
+      for (int c = 0; c < BN / 32; ++c) {
+        if (c * 32 < t.n_i) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(t_row + (uint32_t)(c * 32), v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int row = __shfl_sync(0xffffffffu, cid[c], j);
+            if (row >= 0 && m_ok) {
+              OutT *p = out + (int64_t)row * args.ldc + m;
+              float val = __uint_as_float(v[j]);
+              if (args.accumulate) {
+                val += cvt_in<OutT>(*p);
+                *p = cvt_out<OutT>(val);
+              } else {
+                st_cs(p, cvt_out<OutT>(val));
+              }
+            }
           }
         }
       }
@@ -231,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (my_units == 0) write_zero_rows<OutT>(args, z0, z1, et);
+    if (my_units == 0) write_zero_rows<OutT>(args, z0, z1, ew, lane);
   }
 
   __syncthreads();

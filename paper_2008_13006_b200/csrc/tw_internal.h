@@ -64,6 +64,7 @@ struct GemmArgs {
   int32_t wbytes;     // weight-image bytes per k-block (wrows * 128)
   uint32_t idesc;     // instruction descriptor without the N field
   int32_t block_n;
+  int32_t avg_cols;   // mean live-tile width (zero-row load balancing)
 };
 
 int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,
