@@ -10,6 +10,7 @@
 #include "tw_internal.h"
 
 namespace tw {
+bool use_tma_gather();
 cudaError_t launch_tw_gemm_sm100(const CUtensorMap &tmap, const GemmArgs &args, int out_dtype, int grid,
                                  cudaStream_t stream);
 cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
@@ -179,7 +180,7 @@ int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, 
   }
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  if (n_live > 0) {
+  if (n_live > 0 && use_tma_gather()) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)hp.k};
@@ -199,6 +200,8 @@ int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, 
   a.wimg = p->d_wimg;
   a.out = ct;
   a.ldc = ldc;
+  a.at = at;
+  a.lda = lda;
   a.M = (int32_t)m;
   a.n_live = (int32_t)n_live;
   a.mblocks = (int32_t)((m + 127) / 128);

@@ -1,7 +1,7 @@
 // K2: persistent grouped tile-wise sparse GEMM for sm_100a.
 //
 // Replaces, in one launch, the reference's per-call pipeline
-//   _plan_tasks + gather_rows   (engine.py:61-69, :126-149)  -> TMA gather4 of
+//   _plan_tasks + gather_rows   (engine.py:61-69, :126-149)  -> row gather of
 //                                 the kept A^T rows straight into SW128 smem
 //   group_by_shape + execute_batched + thread pool (engine.py:72-123)
 //                               -> static LPT work list over persistent CTAs
@@ -14,36 +14,43 @@
 // unit), N = the tile's output columns (n_i <= 256), K = the tile's kept rows.
 //   A operand (MN-major, SW128): kept rows of A^T (K x M, M contiguous).  Per
 //     pipeline stage 64 kept k x 128 tokens: two 64-token halves (LBO = 8 KB),
-//     each 64 rows of 128 B (8-row swizzle atoms, SBO = 1 KB).  Loaded with
-//     16 x 2 TMA gather4 (4 kept k-rows each); padded k indices point past K
-//     so TMA zero-fills them.
+//     each 64 rows of 128 B (8-row swizzle atoms, SBO = 1 KB).  Gathered by
+//     the 4 producer warps with 16-byte cp.async (zero-fill for padded rows
+//     and tokens >= M), or -- kGather == kGatherTma -- by TMA gather4.
 //   B operand (K-major, SW128): the packed weight image of the tile, one
-//     1-D bulk copy per stage (wrows x 128 B, pre-swizzled on the host).
+//     1-D TMA bulk copy per stage (wrows x 128 B, pre-swizzled on the host).
 //   D (TMEM, fp32): lane = token, column = tile column.  Double buffered
 //     (2 x BN columns) so the epilogue of unit i overlaps the mainloop of i+1.
 // Epilogue.  tcgen05.ld 32x32b: thread t of epilogue warp q owns token
 //   m0 + 32q + t; for each tile column n the warp stores 32 consecutive
 //   tokens to C^T[col_ids[n], m0 + 32q ...] -- one 128 B coalesced line (fp32).
 //
-// Warp roles (192 threads): w0 = TMA producer, w1 = MMA issuer + TMEM owner,
-// w2..w5 = epilogue (TMEM lane quadrant = warp % 4).
+// Warp roles (288 threads): w0-3 = A gather + W bulk copy (producer),
+// w4 = MMA issuer + TMEM owner, w5-8 = epilogue (TMEM lane quadrant w % 4).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
 
 #include "tw_internal.h"
 #include "tw_ptx.cuh"
 
 namespace tw {
 
-
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kProducerWarps = 4;
+constexpr int kMmaWarp = kProducerWarps;
+constexpr int kEpiWarp0 = kProducerWarps + 1;
+constexpr int kThreads = (kProducerWarps + 1 + 4) * 32;
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;
 constexpr uint32_t kABytes = kBlockM * kBlockK * 2;  // 16 KB per stage
+constexpr int kGatherCpAsync = 0;
+constexpr int kGatherTma = 1;
 
 template <int BN>
 struct Cfg {
@@ -116,7 +123,7 @@ __device__ __forceinline__ int zero_split(const GemmArgs &a, int c, int G, int u
   return (int)min(z, (int64_t)a.n_zero);
 }
 
-template <int BN, typename OutT>
+template <int BN, typename OutT, int kGather>
 __global__ void __launch_bounds__(kThreads, 1)
     tw_gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_at, const __grid_constant__ GemmArgs args) {
   using C = Cfg<BN>;
@@ -135,8 +142,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total_units = args.n_live * args.mblocks;
 
   if (threadIdx.x == 0) {
+    // full: W bulk-copy arrive(+tx) and, for the cp.async gather, one
+    // deferred arrival per producer thread
+    const uint32_t full_count = kGather == kGatherTma ? 1u : 1u + kProducerWarps * 32u;
     for (int s = 0; s < C::kStages; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], full_count);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -144,48 +154,82 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tempty[s], 128);
     }
     ptx::fence_mbar_init();
-    ptx::prefetch_tmap(&tmap_at);
+    if (kGather == kGatherTma) ptx::prefetch_tmap(&tmap_at);
   }
-  if (warp == 1) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
+  if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer (whole warp)
-    // Lane l < 16 owns kept-k rows 4l..4l+3 of each 64-row stage: it loads
-    // their indices one stage ahead (one coalesced 256 B load per stage) and
-    // issues the two gather4 copies (token halves) for them; lane 0 handles
-    // the barriers and the weight-image bulk copy.
+  if (warp < kProducerWarps) {
+    // ------------------------------------------------ producer warps
     const uint64_t keep = ptx::policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
       const TileMeta t = args.tiles[u / args.mblocks];
       const int m0 = (u % args.mblocks) * kBlockM;
-      const int4 *ki = reinterpret_cast<const int4 *>(args.kidx + t.kidx_off);
+      const int32_t *ki = args.kidx + t.kidx_off;
       const uint8_t *wsrc = args.wimg + t.w_off;
-      int4 rows_next = lane < 16 ? __ldg(ki + lane) : make_int4(0, 0, 0, 0);
-      for (int kb = 0; kb < t.nkb; ++kb) {
-        const int4 rows = rows_next;
-        if (kb + 1 < t.nkb && lane < 16) rows_next = __ldg(ki + (kb + 1) * 16 + lane);
-        if (lane == 0) {
+      if (kGather == kGatherTma) {
+        if (warp != 0) continue;
+        // lane l < 16 issues the gather4 pair for kept rows 4l..4l+3 of each
+        // stage, indices loaded one stage ahead
+        int4 rows_next = lane < 16 ? __ldg(reinterpret_cast<const int4 *>(ki) + lane) : make_int4(0, 0, 0, 0);
+        for (int kb = 0; kb < t.nkb; ++kb) {
+          const int4 rows = rows_next;
+          if (kb + 1 < t.nkb && lane < 16) rows_next = __ldg(reinterpret_cast<const int4 *>(ki) + (kb + 1) * 16 + lane);
+          if (lane == 0) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[stage], kABytes + (uint32_t)args.wbytes);
+            ptx::bulk_g2s(sB + stage * C::kBBytes, wsrc + (int64_t)kb * args.wbytes, (uint32_t)args.wbytes,
+                          &full[stage], keep);
+          }
+          __syncwarp();
+          if (lane < 16) {
+            uint8_t *a_dst = sA + stage * kABytes + lane * 512;
+            ptx::tma_gather4(a_dst, &tmap_at, &full[stage], m0, rows, keep);
+            ptx::tma_gather4(a_dst + 8192, &tmap_at, &full[stage], m0 + 64, rows, keep);
+          }
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      } else {
+        // cp.async gather: warp w fills kept rows 16w..16w+15 of the stage.
+        // Per instruction lanes 0-15 copy one row's 256 B token span (both
+        // 64-token halves), lanes 16-31 the next row; 8 instructions/stage.
+        const int j = lane & 15;             // 16-byte chunk within the 256 B span
+        const int half = j >> 3, c = j & 7;  // token half, chunk within the 128 B row
+        const int mcol = m0 + half * 64 + c * 8;
+        const uint32_t src_bytes_m = mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u);
+        const __nv_bfloat16 *at = reinterpret_cast<const __nv_bfloat16 *>(args.at);
+        int idx_next = __ldg(ki + warp * 16 + j);
+        for (int kb = 0; kb < t.nkb; ++kb) {
+          const int idx_mine = idx_next;
+          if (kb + 1 < t.nkb) idx_next = __ldg(ki + (kb + 1) * kBlockK + warp * 16 + j);
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], kABytes + (uint32_t)args.wbytes);
-          ptx::bulk_g2s(sB + stage * C::kBBytes, wsrc + (int64_t)kb * args.wbytes, (uint32_t)args.wbytes,
-                        &full[stage], keep);
+          if (warp == 0 && lane == 0) {
+            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes);
+            ptx::bulk_g2s(sB + stage * C::kBBytes, wsrc + (int64_t)kb * args.wbytes, (uint32_t)args.wbytes,
+                          &full[stage], keep);
+          }
+          uint8_t *a_stage = sA + stage * kABytes + half * 8192;
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rl = it * 2 + (lane >> 4);  // row within this warp's 16
+            const int r = warp * 16 + rl;         // kept row within the stage
+            const int krow = __shfl_sync(0xffffffffu, idx_mine, rl);
+            const bool row_ok = kb * kBlockK + r < t.k_i;
+            const uint32_t nbytes = row_ok ? src_bytes_m : 0u;
+            const __nv_bfloat16 *src = at + (row_ok ? (int64_t)krow * args.lda + (nbytes ? mcol : 0) : 0);
+            ptx::cp_async_16(a_stage + r * 128 + ((c ^ (r & 7)) * 16), src, nbytes);
+          }
+          ptx::cp_async_mbar_arrive_noinc(&full[stage]);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (lane < 16) {
-          uint8_t *a_dst = sA + stage * kABytes + lane * 512;
-          ptx::tma_gather4(a_dst, &tmap_at, &full[stage], m0, rows, keep);
-          ptx::tma_gather4(a_dst + 8192, &tmap_at, &full[stage], m0 + 64, rows, keep);
-        }
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------ MMA issuer
     int stage = 0;
     uint32_t phase = 0;
@@ -202,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       for (int kb = 0; kb < t.nkb; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
+        if (kGather == kGatherCpAsync) ptx::fence_proxy_async_smem();  // cp.async wrote via the generic proxy
         ptx::tc_fence_after();
         const int nk = min(4, t.k16 - kb * 4);
         if (ptx::elect_one()) {
@@ -223,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------ epilogue (128 threads)
     const int q = warp & 3;   // TMEM lane quadrant this warp may access
-    const int ew = warp - 2;  // 0..3
+    const int ew = warp - kEpiWarp0;  // 0..3
     const int G = gridDim.x;
     const int64_t row_bytes = (int64_t)args.M * sizeof(OutT);
     const int64_t unit_bytes = (int64_t)kBlockM * args.avg_cols * sizeof(OutT);
@@ -257,11 +302,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_ld_32x32b_x32(t_row + (uint32_t)(c * 32), v);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int row = __shfl_sync(0xffffffffu, cid[c], j);
+          for (int jj = 0; jj < 32; ++jj) {
+            const int row = __shfl_sync(0xffffffffu, cid[c], jj);
             if (row >= 0 && m_ok) {
               OutT *p = out + (int64_t)row * args.ldc + m;
-              float val = __uint_as_float(v[j]);
+              float val = __uint_as_float(v[jj]);
               if (args.accumulate) {
                 val += cvt_in<OutT>(*p);
                 *p = cvt_out<OutT>(val);
@@ -281,15 +326,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
-template <int BN, typename OutT>
+template <int BN, typename OutT, int kGather>
 cudaError_t launch_bn(const CUtensorMap &tmap, const GemmArgs &args, int grid, cudaStream_t stream) {
-  auto kern = tw_gemm_sm100_kernel<BN, OutT>;
+  auto kern = tw_gemm_sm100_kernel<BN, OutT, kGather>;
   const int smem = (int)Cfg<BN>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -297,22 +342,37 @@ cudaError_t launch_bn(const CUtensorMap &tmap, const GemmArgs &args, int grid, c
   return cudaGetLastError();
 }
 
-template <typename OutT>
+template <typename OutT, int kGather>
 cudaError_t launch_out(const CUtensorMap &tmap, const GemmArgs &args, int grid, cudaStream_t stream) {
-  return args.block_n <= 128 ? launch_bn<128, OutT>(tmap, args, grid, stream)
-                             : launch_bn<256, OutT>(tmap, args, grid, stream);
+  return args.block_n <= 128 ? launch_bn<128, OutT, kGather>(tmap, args, grid, stream)
+                             : launch_bn<256, OutT, kGather>(tmap, args, grid, stream);
+}
+
+template <int kGather>
+cudaError_t launch_gather(const CUtensorMap &tmap, const GemmArgs &args, int out_dtype, int grid,
+                          cudaStream_t stream) {
+  switch (out_dtype) {
+    case TW_F32: return launch_out<float, kGather>(tmap, args, grid, stream);
+    case TW_BF16: return launch_out<__nv_bfloat16, kGather>(tmap, args, grid, stream);
+    case TW_F16: return launch_out<__half, kGather>(tmap, args, grid, stream);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
+bool use_tma_gather() {
+  static const bool v = [] {
+    const char *e = std::getenv("TW_B200_GATHER");
+    return e && std::strcmp(e, "tma") == 0;
+  }();
+  return v;
+}
+
 cudaError_t launch_tw_gemm_sm100(const CUtensorMap &tmap, const GemmArgs &args, int out_dtype, int grid,
                                  cudaStream_t stream) {
-  switch (out_dtype) {
-    case TW_F32: return launch_out<float>(tmap, args, grid, stream);
-    case TW_BF16: return launch_out<__nv_bfloat16>(tmap, args, grid, stream);
-    case TW_F16: return launch_out<__half>(tmap, args, grid, stream);
-  }
-  return cudaErrorInvalidValue;
+  return use_tma_gather() ? launch_gather<kGatherTma>(tmap, args, out_dtype, grid, stream)
+                          : launch_gather<kGatherCpAsync>(tmap, args, out_dtype, grid, stream);
 }
 
 }  // namespace tw

@@ -56,6 +56,8 @@ struct GemmArgs {
   const uint8_t *wimg;
   void *out;
   int64_t ldc;
+  const void *at;     // A^T (K x M, 16-bit), row stride lda (cp.async gather path)
+  int64_t lda;
   int32_t M;
   int32_t n_live;
   int32_t mblocks;
