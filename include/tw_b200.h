@@ -182,6 +182,13 @@ int tw_gemm_tew(const tw_plan *plan, const void *at, int64_t m, int64_t lda, con
                 const int32_t *row_idx, const float *values, int64_t nnz, void *ct, int64_t ldc,
                 int out_dtype, void *stream);
 
+/* Profiling hook: tw_gemm (accumulate = 0) that also records %globaltimer
+ * stamps into the device buffer trace[grid * 8 units * 8 slots] (int64, ns;
+ * slots: producer unit start / issued, MMA start / committed, epilogue zero
+ * rows done / accumulator ready / unit stored).  Not for production use. */
+int tw_gemm_traced(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
+                   int out_dtype, int64_t *trace, void *stream);
+
 /* Number of SMs used by the persistent grid on the current device. */
 int tw_device_sm_count(int *sms);
 

@@ -154,8 +154,22 @@ int tw_plan_destroy(tw_plan *p) {
   return TW_OK;
 }
 
+static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
+                     int out_dtype, int accumulate, int64_t *trace, void *stream);
+
 int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
             int accumulate, void *stream) {
+  return gemm_impl(p, at, m, lda, ct, ldc, out_dtype, accumulate, nullptr, stream);
+}
+
+int tw_gemm_traced(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
+                   int64_t *trace, void *stream) {
+  if (!trace) return fail(TW_ERR_ARG, "null trace buffer");
+  return gemm_impl(p, at, m, lda, ct, ldc, out_dtype, 0, trace, stream);
+}
+
+static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
+                     int out_dtype, int accumulate, int64_t *trace, void *stream) {
   clear_error();
   if (!p) return fail(TW_ERR_ARG, "null plan");
   if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan (tw_plan_build_host) cannot run on the GPU");
@@ -214,6 +228,7 @@ int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, 
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 15) | ((128u >> 4) << 24);
   a.block_n = hp.block_n;
   a.avg_cols = n_live > 0 ? (int32_t)(hp.sum_n / n_live) : 0;
+  a.trace = trace;
   const int64_t units = n_live * a.mblocks;
   const int64_t zero_bytes = (int64_t)a.n_zero * m * out_size(out_dtype);
   int64_t grid = units;

@@ -109,6 +109,17 @@ __device__ __forceinline__ void write_zero_rows(const GemmArgs &a, int r0, int r
   }
 }
 
+// Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
+// Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
+// committed, 4 epilogue zero rows done, 5 accumulator ready, 6 unit stored.
+__device__ __forceinline__ void trace_evt(const GemmArgs &a, int unit_i, int slot) {
+  if (a.trace != nullptr && unit_i < 8) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[((int64_t)blockIdx.x * 8 + unit_i) * 8 + slot] = (int64_t)t;
+  }
+}
+
 // First zero-list row owned by CTA c: zero rows are dealt out so that every
 // CTA writes about the same number of output bytes (its MMA units' columns
 // plus its zero rows), i.e. CTAs with one unit fewer take more zero rows.
@@ -167,8 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t keep = ptx::policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    int ui = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++ui) {
       const TileMeta t = args.tiles[u / args.mblocks];
+      if (threadIdx.x == 0) trace_evt(args, ui, 0);
       const int m0 = (u % args.mblocks) * kBlockM;
       const int32_t *ki = args.kidx + t.kidx_off;
       const uint8_t *wsrc = args.wimg + t.w_off;
@@ -227,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::cp_async_mbar_arrive_noinc(&full[stage]);
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
+        if (threadIdx.x == 0) trace_evt(args, ui, 1);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -237,13 +251,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     const uint32_t a_base = ptx::smem_u32(sA);
     const uint32_t b_base = ptx::smem_u32(sB);
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    int ui = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++ui) {
       const TileMeta t = args.tiles[u / args.mblocks];
       const uint32_t n_mma = (uint32_t)((t.n_i + 15) & ~15);
       const uint32_t idesc = args.idesc | ((n_mma >> 3) << 17);
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
+      if (lane == 0) trace_evt(args, ui, 2);
       for (int kb = 0; kb < t.nkb; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         if (kGather == kGatherCpAsync) ptx::fence_proxy_async_smem();  // cp.async wrote via the generic proxy
@@ -262,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
       __syncwarp();
+      if (lane == 0) trace_evt(args, ui, 3);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -290,10 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         cid[c] = (c * 32 + lane < t.n_i) ? __ldg(args.colids + t.col_off + c * 32 + lane) : -1;
       // zero part i of my_units (written while unit i's mainloop runs)
       write_zero_rows<OutT>(args, z0 + (z1 - z0) * i / my_units, z0 + (z1 - z0) * (i + 1) / my_units, ew, lane);
+      if (ew == 0 && lane == 0) trace_evt(args, i, 4);
       const int m = (u % args.mblocks) * kBlockM + q * 32 + lane;
       const bool m_ok = m < args.M;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      if (ew == 0 && lane == 0) trace_evt(args, i, 5);
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
@@ -319,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
+      if (ew == 0 && lane == 0) trace_evt(args, i, 6);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }

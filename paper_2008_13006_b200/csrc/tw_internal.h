@@ -67,6 +67,7 @@ struct GemmArgs {
   uint32_t idesc;     // instruction descriptor without the N field
   int32_t block_n;
   int32_t avg_cols;   // mean live-tile width (zero-row load balancing)
+  int64_t *trace;     // optional per-CTA event timeline (tw_gemm_traced), else null
 };
 
 int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,

@@ -1,0 +1,83 @@
+"""Per-CTA / per-unit timeline of one tw_gemm launch (tw_gemm_traced hook).
+
+    python tools/trace_units.py --workload C2a [--out-dtype fp32]
+
+Prints, relative to the earliest stamp in the launch: when each role starts
+and finishes its units, so stalls can be attributed to the producer (gather),
+the MMA issuer or the epilogue (stores / zero rows).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2008_13006_b200 as tw  # noqa: E402
+from paper_2008_13006_b200 import _lib  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+
+SLOTS = ["prod_start", "prod_issued", "mma_start", "mma_commit", "epi_zero_done", "epi_acc_ready", "epi_stored"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="C2a")
+    ap.add_argument("--out-dtype", default="fp32")
+    ap.add_argument("--json", default=None)
+    args = ap.parse_args()
+    m, k, n, g, s, _ = bench.WORKLOADS[args.workload]
+    a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), bench.to_pattern(tw, p))
+    plan = tw.TwPlan(ts)
+    at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
+    dt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[args.out_dtype]
+    out = torch.empty((n, m), dtype=dt, device="cuda")
+    sms = ctypes.c_int(0)
+    _lib.call("tw_device_sm_count", ctypes.byref(sms))
+    trace = torch.zeros(sms.value * 64, dtype=torch.int64, device="cuda")
+    code = {"fp32": 0, "bf16": 1, "fp16": 2}[args.out_dtype]
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(5):
+        plan.gemm(at, out=out, out_dtype=dt)
+    torch.cuda.synchronize()
+    trace.zero_()
+    _lib.call("tw_gemm_traced", plan._h, at.data_ptr(), m, at.stride(0), out.data_ptr(), out.stride(0), code,
+              trace.data_ptr(), stream)
+    torch.cuda.synchronize()
+    tr = trace.cpu().numpy().reshape(sms.value, 8, 8).astype(np.float64)
+    valid = tr > 0
+    t0 = tr[valid].min()
+    rel = np.where(valid, (tr - t0) / 1e3, np.nan)  # us
+    print(f"launch span {np.nanmax(rel):.2f} us over {sms.value} CTAs")
+    summary = {}
+    for si, name in enumerate(SLOTS):
+        for ui in range(4):
+            col = rel[:, ui, si]
+            if np.isfinite(col).any():
+                summary[f"u{ui}.{name}"] = [float(np.nanmin(col)), float(np.nanmedian(col)), float(np.nanmax(col))]
+    for kk, v in summary.items():
+        print(f"{kk:22s} min {v[0]:8.2f}  med {v[1]:8.2f}  max {v[2]:8.2f}")
+    # per-unit durations
+    mma = rel[:, :, 3] - rel[:, :, 2]
+    prod = rel[:, :, 1] - rel[:, :, 0]
+    store = rel[:, :, 6] - rel[:, :, 5]
+    print(f"producer issue time/unit med {np.nanmedian(prod):.2f} us; MMA issue/unit med {np.nanmedian(mma):.2f}; "
+          f"epilogue store/unit med {np.nanmedian(store):.2f}")
+    if args.json:
+        with open(args.json, "w") as f:
+            json.dump({"summary": summary, "raw_us": np.nan_to_num(rel, nan=-1).tolist()}, f)
+
+
+if __name__ == "__main__":
+    main()
