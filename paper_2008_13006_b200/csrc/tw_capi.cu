@@ -1,18 +1,16 @@
-// C ABI (include/tw_b200.h): plan upload, TMA descriptor creation and the
-// launch wrappers of libtw_b200.so.
-#include <cuda.h>
+// C ABI (include/tw_b200.h): plan upload, argument checking and the launch
+// wrappers of libtw_b200.so.
 #include <cuda_runtime.h>
 
 #include <cstring>
-#include <mutex>
+#include <new>
 #include <string>
 
 #include "tw_internal.h"
 
 namespace tw {
-bool use_tma_gather();
-cudaError_t launch_tw_gemm_sm100(const CUtensorMap &tmap, const GemmArgs &args, int out_dtype, int grid,
-                                 cudaStream_t stream);
+int tokens_per_unit(int block_n);
+cudaError_t launch_tw_gemm_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream);
 cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
                         cudaStream_t s);
 cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t lda, int64_t col_begin, int64_t n_cols,
@@ -26,23 +24,6 @@ namespace {
 
 int cuda_fail(cudaError_t e, const char *what) {
   return fail(TW_ERR_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
-}
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
 }
 
 int sm_count_of_current(int *sms, int *major) {
@@ -190,21 +171,7 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
     if (!at) return fail(TW_ERR_ARG, "null activations");
     if (lda < m) return fail(TW_ERR_DIMENSION, "lda < M");
     if (lda % 8 != 0 || (reinterpret_cast<uintptr_t>(at) & 15) != 0)
-      return fail(TW_ERR_ARG, "activations need lda % 8 == 0 and a 16-byte aligned base (TMA)");
-  }
-  CUtensorMap tmap;
-  std::memset(&tmap, 0, sizeof(tmap));
-  if (n_live > 0 && use_tma_gather()) {
-    EncodeTiledFn enc = get_encode();
-    if (!enc) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)hp.k};
-    cuuint64_t strides[1] = {(cuuint64_t)lda * 2};
-    cuuint32_t box[2] = {64, 1};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(&tmap, hp.in_dtype == TW_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                     2, const_cast<void *>(at), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+      return fail(TW_ERR_ARG, "activations need lda % 8 == 0 and a 16-byte aligned base (16-byte row gathers)");
   }
   GemmArgs a{};
   a.tiles = p->d_tiles;
@@ -218,7 +185,8 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.lda = lda;
   a.M = (int32_t)m;
   a.n_live = (int32_t)n_live;
-  a.mblocks = (int32_t)((m + 127) / 128);
+  const int tb = tokens_per_unit(hp.block_n);
+  a.mblocks = (int32_t)((m + tb - 1) / tb);
   a.n_zero = accumulate ? 0 : (int32_t)hp.zero_rows.size();
   a.accumulate = accumulate ? 1 : 0;
   a.wbytes = hp.wrows * 128;
@@ -236,7 +204,7 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   if (zero_ctas > grid) grid = zero_ctas;
   if (grid > sms) grid = sms;
   if (grid < 1) grid = 1;
-  cudaError_t e = launch_tw_gemm_sm100(tmap, a, out_dtype, (int)grid, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_tw_gemm_sm100(a, out_dtype, (int)grid, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tw_gemm launch");
   return TW_OK;
 }
