@@ -151,6 +151,15 @@ __device__ __forceinline__ void trace_evt(const GemmArgs &a, int unit_i, int slo
     a.trace[((int64_t)blockIdx.x * 8 + unit_i) * 8 + slot] = (int64_t)t;
   }
 }
+// per pipeline stage (first 32 of each CTA), after the unit table:
+// slot 0 producer issued, 1 MMA saw it full, 2 MMA committed
+__device__ __forceinline__ void trace_stage(const GemmArgs &a, int s, int slot) {
+  if (a.trace != nullptr && s < 32) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[(int64_t)gridDim.x * 64 + ((int64_t)blockIdx.x * 32 + s) * 4 + slot] = (int64_t)t;
+  }
+}
 
 // First zero-list row owned by CTA c: zero rows are dealt out so that every
 // CTA writes about the same number of output bytes (its MMA units' columns
@@ -207,46 +216,55 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // ------------------------------------------------ producer warps
     // Warp w fills kept rows 16w..16w+15 of each 64-row stage.  A row's TB
     // tokens are TB/8 16-byte chunks; one instruction covers 32/(TB/8) rows.
+    // Address work per copy is one shuffle of the row's byte offset plus a
+    // 64-bit add: the row offsets (kept index * row pitch) are computed once
+    // per stage by 16 lanes, one stage ahead, and the swizzled smem offset of
+    // iteration `it` is a per-lane constant (row & 7 == it & 7).
     constexpr int kChunks = TB / 8;
     constexpr int kRowsPerInst = 32 / kChunks;
     const int chunk = lane % kChunks;
     const int rsub = lane / kChunks;
     const int blk = chunk >> 3, cc = chunk & 7;  // 64-token block, 16 B chunk in the 128 B row
     const uint64_t keep = ptx::policy_evict_last();
-    const __nv_bfloat16 *at = reinterpret_cast<const __nv_bfloat16 *>(args.at);
+    const char *at_bytes = reinterpret_cast<const char *>(args.at);
+    const int64_t pitch = args.lda * 2;
     int stage = 0;
     uint32_t phase = 0;
-    int ui = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++ui) {
-      const TileMeta t = args.tiles[u / args.mblocks];
+    int ui = 0, sc = 0;
+    int u = blockIdx.x;
+    TileMeta t_next = u < total_units ? args.tiles[u / args.mblocks] : TileMeta{};
+    for (; u < total_units; u += gridDim.x, ++ui) {
+      const TileMeta t = t_next;
+      if (u + (int)gridDim.x < total_units) t_next = args.tiles[(u + gridDim.x) / args.mblocks];
       if (threadIdx.x == 0) trace_evt(args, ui, 0);
       const int m0 = (u % args.mblocks) * TB;
       const int mcol = m0 + chunk * 8;
       const uint32_t src_bytes_m = mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u);
-      const int32_t *ki = args.kidx + t.kidx_off;
+      const char *lane_base = at_bytes + (src_bytes_m ? (int64_t)mcol * 2 : 0);
+      const int32_t *ki = args.kidx + t.kidx_off + warp * 16 + (lane & 15);
       const uint8_t *wsrc = args.wimg + t.w_off;
-      int idx_next = __ldg(ki + warp * 16 + (lane & 15));
+      int64_t off_next = (int64_t)__ldg(ki) * pitch;
       for (int kb = 0; kb < t.nkb; ++kb) {
-        const int idx_mine = idx_next;
-        if (kb + 1 < t.nkb) idx_next = __ldg(ki + (kb + 1) * kBlockK + warp * 16 + (lane & 15));
+        const int64_t off_mine = off_next;
+        if (kb + 1 < t.nkb) off_next = (int64_t)__ldg(ki + (kb + 1) * kBlockK) * pitch;
+        const int rows_valid = t.k_i - kb * kBlockK - warp * 16;  // rows of this warp holding real kept k
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (warp == 0 && lane == 0) {
           ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes);
           ptx::bulk_g2s(sB + stage * C::kBBytes, wsrc + (int64_t)kb * args.wbytes, (uint32_t)args.wbytes,
                         &full[stage], keep);
         }
-        uint8_t *a_stage = sA + stage * C::kABytes + blk * 8192;
+        uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + warp * 16 * 128;
 #pragma unroll
         for (int it = 0; it < 16 / kRowsPerInst; ++it) {
-          const int rl = it * kRowsPerInst + rsub;  // row within this warp's 16
-          const int r = warp * 16 + rl;             // kept row within the stage
-          const int krow = __shfl_sync(0xffffffffu, idx_mine, rl);
-          const bool row_ok = kb * kBlockK + r < t.k_i;
-          const uint32_t nbytes = row_ok ? src_bytes_m : 0u;
-          const __nv_bfloat16 *src = at + (row_ok ? (int64_t)krow * args.lda + (nbytes ? mcol : 0) : 0);
-          ptx::cp_async_16(a_stage + r * 128 + ((cc ^ (r & 7)) * 16), src, nbytes);
+          const int rl = it * kRowsPerInst + rsub;  // row within this warp's 16 (rl & 7 == (it*kRowsPerInst) & 7 + rsub)
+          const int64_t roff = __shfl_sync(0xffffffffu, off_mine, rl);
+          const uint32_t nbytes = rl < rows_valid ? src_bytes_m : 0u;
+          ptx::cp_async_16(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), nbytes ? lane_base + roff : at_bytes, nbytes);
         }
         ptx::cp_async_mbar_arrive_noinc(&full[stage]);
+        if (threadIdx.x == 0) trace_stage(args, sc, 0);
+        ++sc;
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
       if (threadIdx.x == 0) trace_evt(args, ui, 1);
@@ -259,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     uint32_t acc_phase = 0;
     const uint32_t a_base = ptx::smem_u32(sA);
     const uint32_t b_base = ptx::smem_u32(sB);
-    int ui = 0;
+    int ui = 0, sc = 0;
     for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++ui) {
       const TileMeta t = args.tiles[u / args.mblocks];
       const uint32_t n_mma = (uint32_t)((t.n_i + 15) & ~15);
@@ -270,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (lane == 0) trace_evt(args, ui, 2);
       for (int kb = 0; kb < t.nkb; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
+        if (lane == 0) trace_stage(args, sc, 1);
         ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
         ptx::tc_fence_after();
         const int nk = min(4, t.k16 - kb * 4);
@@ -286,6 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
           ptx::mma_commit(&empty[stage]);
         }
         __syncwarp();
+        if (lane == 0) trace_stage(args, sc, 2);
+        ++sc;
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
       if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);

@@ -45,7 +45,7 @@ def main():
     out = torch.empty((n, m), dtype=dt, device="cuda")
     sms = ctypes.c_int(0)
     _lib.call("tw_device_sm_count", ctypes.byref(sms))
-    trace = torch.zeros(sms.value * 64, dtype=torch.int64, device="cuda")
+    trace = torch.zeros(sms.value * (64 + 128), dtype=torch.int64, device="cuda")
     code = {"fp32": 0, "bf16": 1, "fp16": 2}[args.out_dtype]
     stream = torch.cuda.current_stream().cuda_stream
     for _ in range(5):
@@ -55,7 +55,9 @@ def main():
     _lib.call("tw_gemm_traced", plan._h, at.data_ptr(), m, at.stride(0), out.data_ptr(), out.stride(0), code,
               trace.data_ptr(), stream)
     torch.cuda.synchronize()
-    tr = trace.cpu().numpy().reshape(sms.value, 8, 8).astype(np.float64)
+    full = trace.cpu().numpy().astype(np.float64)
+    tr = full[: sms.value * 64].reshape(sms.value, 8, 8)
+    st = full[sms.value * 64:].reshape(sms.value, 32, 4)
     valid = tr > 0
     t0 = tr[valid].min()
     rel = np.where(valid, (tr - t0) / 1e3, np.nan)  # us
@@ -68,6 +70,12 @@ def main():
                 summary[f"u{ui}.{name}"] = [float(np.nanmin(col)), float(np.nanmedian(col)), float(np.nanmax(col))]
     for kk, v in summary.items():
         print(f"{kk:22s} min {v[0]:8.2f}  med {v[1]:8.2f}  max {v[2]:8.2f}")
+    srel = np.where(st > 0, (st - t0) / 1e3, np.nan)
+    print("stage  issued(med)  full(med)  committed(med)   [CTA 0: issued full committed]")
+    for si in range(14):
+        c0 = srel[0, si]
+        print(f"{si:5d} {np.nanmedian(srel[:, si, 0]):9.2f} {np.nanmedian(srel[:, si, 1]):9.2f} "
+              f"{np.nanmedian(srel[:, si, 2]):9.2f}     [{c0[0]:7.2f} {c0[1]:7.2f} {c0[2]:7.2f}]")
     # per-unit durations
     mma = rel[:, :, 3] - rel[:, :, 2]
     prod = rel[:, :, 1] - rel[:, :, 0]
