@@ -49,6 +49,7 @@ SIGNATURES = {
     "tw_plan_destroy": (_i32, [_p]),
     "tw_plan_get_info": (_i32, [_p, ctypes.POINTER(PlanInfo)]),
     "tw_plan_export": (_i32, [_p, _i32, _p, _pi64]),
+    "tw_schedule_export": (_i32, [_p, _i64, _i32, _i32, _i32, _i32, _p, _pi64]),
     "tw_gemm": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _i32, _p]),
     "tw_gemm_traced": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _p, _p]),
     "tw_gemm_exact": (_i32, [_p, _p, _i64, _i64, _p, _i64, _p]),

@@ -23,7 +23,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libtw_b200.so")
 
-SOURCES = ["tw_pack.cpp", "tw_capi.cu", "tw_gemm_sm100.cu", "tw_aux.cu"]
+SOURCES = ["tw_pack.cpp", "tw_schedule.cpp", "tw_capi.cu", "tw_gemm_sm100.cu", "tw_aux.cu"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

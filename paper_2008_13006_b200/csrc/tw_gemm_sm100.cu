@@ -4,15 +4,16 @@
 //   _plan_tasks + gather_rows   (engine.py:61-69, :126-149)  -> cp.async row
 //                                 gather of the kept A^T rows into SW128 smem
 //   group_by_shape + execute_batched + thread pool (engine.py:72-123)
-//                               -> static LPT work list over persistent CTAs
+//                               -> static per-CTA unit lists (host LPT,
+//                                  tw_schedule.cpp) over persistent CTAs
 //   mm_accum                    (_kernels.py:13-27) -> tcgen05.mma, fp32 TMEM
 //   ct = zeros(N, M)            (engine.py:102) -> pruned C^T rows written as
-//                                 zeros by the epilogue, interleaved with the
-//                                 MMA work
+//                                 zeros by the epilogue while it waits for
+//                                 accumulators
 //
-// Work unit = (live tile, block of TB tokens).  TB = 256 for tiles up to 128
-// columns (two M=128 MMAs per k-step share the weight operand), TB = 128 for
-// G = 256 (one M=128, N<=256 MMA).
+// Work unit = (live tile, token block of nh x 128 tokens).  For tiles of up
+// to 128 columns a unit has up to 256 tokens (two M=128 MMAs per k-step share
+// the weight operand); for G = 256 a unit is 128 tokens x up to 256 columns.
 //   A operand (MN-major, SW128): kept rows of A^T (K x M, M contiguous).  Per
 //     pipeline stage 64 kept k x TB tokens, stored as TB/64 blocks of
 //     [64 rows x 128 B] (8-row swizzle atoms: SBO = 1 KB, blocks LBO = 8 KB).
@@ -21,13 +22,12 @@
 //   B operand (K-major, SW128): the packed weight image of the tile, one
 //     1-D TMA bulk copy per stage (wrows x 128 B, pre-swizzled on the host).
 //   D (TMEM, fp32): 2 x 256 columns (double buffered accumulators).
-// Epilogue (8 warps).  The output C^T has one 16 KB row per output column, so
-// a unit's results are TB-token segments of scattered rows.  Writing them
-// straight from the TMEM register layout (one token per lane) makes every
-// store instruction hit a different row, which measured at 1.7-1.9 TB/s
-// (tools/membench2.cu).  Instead each 32-column chunk is staged through
-// shared memory and written back row by row, 16 B per lane, so one warp
-// instruction covers 512 B of a single row (4.8 TB/s in the same benchmark).
+// Epilogue (8 warps).  The output C^T has one row per output column, so a
+// unit's results are token segments of scattered rows.  Storing straight from
+// the TMEM register layout (one token per lane) makes every store
+// instruction hit a different row (1.7-1.9 TB/s in tools/membench2.cu);
+// instead each 32-column chunk is staged through shared memory and written
+// row by row, 16 B per lane, 512 B of one row per warp instruction (4.8 TB/s).
 //
 // Warp roles (416 threads): w0-3 producer (A gather + W bulk copy), w4 MMA
 // issuer + TMEM owner, w5-12 epilogue (TMEM lane quadrant = warp % 4).
@@ -54,14 +54,14 @@ constexpr int kEpiBarrier = 1;  // named barrier id for the epilogue warps
 
 template <int BN>
 struct Cfg {
-  static constexpr int TB = BN <= 128 ? 256 : 128;           // tokens per unit
-  static constexpr int kHalves = TB / 128;                    // M=128 MMAs per k-step
+  static constexpr int TB = BN <= 128 ? 256 : 128;           // max tokens per unit
+  static constexpr int kHalves = TB / 128;                    // max M=128 MMAs per k-step
   static constexpr uint32_t kABytes = TB * kBlockK * 2;       // 32 KB | 16 KB
   static constexpr uint32_t kBBytes = BN * 128;               // 16 KB | 32 KB
   static constexpr int kStages = 4;
   static constexpr uint32_t kAccCols = 256;                   // TMEM columns per accumulator
   static constexpr uint32_t kTmemCols = 2 * kAccCols;
-  static constexpr int kStageCols = 32 * kHalves == 64 ? 32 : 64;  // staged C^T rows per chunk
+  static constexpr int kStageCols = kHalves == 2 ? 32 : 64;   // staged C^T rows per chunk
   static constexpr uint32_t kStageBytes = 32768;              // chunk staging buffer (fp32)
   static constexpr uint32_t kSmem =
       1024 /*align slack*/ + kStages * (kABytes + kBBytes) + kStageBytes + 1024 /*col ids*/ + 256 /*barriers*/;
@@ -121,29 +121,21 @@ __device__ __forceinline__ void unpack16_add(uint4 old, float *v) {
   }
 }
 
-// Zero rows [r0, r1) of the zero list (pruned columns of C), full M, by the
-// 8 epilogue warps: warp e writes rows r0+e, r0+e+8, ... with coalesced
-// 16-byte streaming stores (512 B per warp instruction).
+// One zero row (a pruned column of C) written by one warp: coalesced 16-byte
+// streaming stores, 512 B per instruction.
 template <typename OutT>
-__device__ __forceinline__ void write_zero_rows(const GemmArgs &a, int r0, int r1, int e, int lane, bool vec) {
+__device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int lane, bool vec) {
+  OutT *base = reinterpret_cast<OutT *>(a.out) + (int64_t)row * a.ldc;
   const int64_t n16 = vec ? (int64_t)a.M * (int64_t)sizeof(OutT) / 16 : 0;
-  const int64_t tail0 = n16 * 16 / (int64_t)sizeof(OutT);
-  int r = r0 + e;
-  int row = r < r1 ? __ldg(a.zero_rows + r) : 0;
-  for (; r < r1; r += kEpiWarps) {
-    const int next = (r + kEpiWarps < r1) ? __ldg(a.zero_rows + r + kEpiWarps) : 0;
-    OutT *base = reinterpret_cast<OutT *>(a.out) + (int64_t)row * a.ldc;
-    uint4 *b16 = reinterpret_cast<uint4 *>(base);
-    const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int64_t i = lane; i < n16; i += 32) __stcs(b16 + i, z);
-    for (int64_t i = tail0 + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(0.f);
-    row = next;
-  }
+  uint4 *b16 = reinterpret_cast<uint4 *>(base);
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int64_t i = lane; i < n16; i += 32) __stcs(b16 + i, z);
+  for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(0.f);
 }
 
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
-// committed, 4 epilogue zero rows done, 5 accumulator ready, 6 unit stored.
+// committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
 __device__ __forceinline__ void trace_evt(const GemmArgs &a, int unit_i, int slot) {
   if (a.trace != nullptr && unit_i < 8) {
     uint64_t t;
@@ -159,20 +151,6 @@ __device__ __forceinline__ void trace_stage(const GemmArgs &a, int s, int slot) 
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[(int64_t)gridDim.x * 64 + ((int64_t)blockIdx.x * 32 + s) * 4 + slot] = (int64_t)t;
   }
-}
-
-// First zero-list row owned by CTA c: zero rows are dealt out so that every
-// CTA writes about the same number of output bytes (its MMA units' columns
-// plus its zero rows), i.e. CTAs with one unit fewer take more zero rows.
-__device__ __forceinline__ int zero_split(const GemmArgs &a, int c, int G, int units, int64_t unit_bytes,
-                                          int64_t row_bytes) {
-  if (c >= G) return a.n_zero;
-  const int64_t q = units / G, rem = units % G;
-  const int64_t before = (int64_t)c * q + min((int64_t)c, rem);
-  const int64_t total = (int64_t)units * unit_bytes + (int64_t)a.n_zero * row_bytes;
-  const int64_t want = total / G * c - before * unit_bytes;
-  int64_t z = want <= 0 ? 0 : want / row_bytes;
-  return (int)min(z, (int64_t)a.n_zero);
 }
 
 template <int BN, typename OutT>
@@ -193,7 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int total_units = args.n_live * args.mblocks;
+  const int u_begin = __ldg(args.sched_off + blockIdx.x);
+  const int u_end = __ldg(args.sched_off + blockIdx.x + 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -218,8 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // tokens are TB/8 16-byte chunks; one instruction covers 32/(TB/8) rows.
     // Address work per copy is one shuffle of the row's byte offset plus a
     // 64-bit add: the row offsets (kept index * row pitch) are computed once
-    // per stage by 16 lanes, one stage ahead, and the swizzled smem offset of
-    // iteration `it` is a per-lane constant (row & 7 == it & 7).
+    // per stage by 16 lanes, one stage ahead.
     constexpr int kChunks = TB / 8;
     constexpr int kRowsPerInst = 32 / kChunks;
     const int chunk = lane % kChunks;
@@ -230,16 +208,18 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int64_t pitch = args.lda * 2;
     int stage = 0;
     uint32_t phase = 0;
-    int ui = 0, sc = 0;
-    int u = blockIdx.x;
-    TileMeta t_next = u < total_units ? args.tiles[u / args.mblocks] : TileMeta{};
-    for (; u < total_units; u += gridDim.x, ++ui) {
-      const TileMeta t = t_next;
-      if (u + (int)gridDim.x < total_units) t_next = args.tiles[(u + gridDim.x) / args.mblocks];
-      if (threadIdx.x == 0) trace_evt(args, ui, 0);
-      const int m0 = (u % args.mblocks) * TB;
+    int sc = 0;
+    int4 su_next = u_begin < u_end ? __ldg(args.sched + u_begin) : make_int4(0, 0, 0, 0);
+    for (int j = u_begin; j < u_end; ++j) {
+      const int4 su = su_next;
+      if (j + 1 < u_end) su_next = __ldg(args.sched + j + 1);
+      const TileMeta t = args.tiles[su.x];
+      if (threadIdx.x == 0) trace_evt(args, j - u_begin, 0);
+      const int m0 = su.y;
+      const bool active = chunk < su.z * 16;  // token half present in this unit
       const int mcol = m0 + chunk * 8;
-      const uint32_t src_bytes_m = mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u);
+      const uint32_t src_bytes_m =
+          !active ? 0u : (mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u));
       const char *lane_base = at_bytes + (src_bytes_m ? (int64_t)mcol * 2 : 0);
       const int32_t *ki = args.kidx + t.kidx_off + warp * 16 + (lane & 15);
       const uint8_t *wsrc = args.wimg + t.w_off;
@@ -257,17 +237,17 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + warp * 16 * 128;
 #pragma unroll
         for (int it = 0; it < 16 / kRowsPerInst; ++it) {
-          const int rl = it * kRowsPerInst + rsub;  // row within this warp's 16 (rl & 7 == (it*kRowsPerInst) & 7 + rsub)
+          const int rl = it * kRowsPerInst + rsub;  // row within this warp's 16
           const int64_t roff = __shfl_sync(0xffffffffu, off_mine, rl);
           const uint32_t nbytes = rl < rows_valid ? src_bytes_m : 0u;
-          ptx::cp_async_16(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), nbytes ? lane_base + roff : at_bytes, nbytes);
+          if (active) ptx::cp_async_16(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), nbytes ? lane_base + roff : at_bytes, nbytes);
         }
         ptx::cp_async_mbar_arrive_noinc(&full[stage]);
         if (threadIdx.x == 0) trace_stage(args, sc, 0);
         ++sc;
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
-      if (threadIdx.x == 0) trace_evt(args, ui, 1);
+      if (threadIdx.x == 0) trace_evt(args, j - u_begin, 1);
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------ MMA issuer
@@ -277,15 +257,16 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     uint32_t acc_phase = 0;
     const uint32_t a_base = ptx::smem_u32(sA);
     const uint32_t b_base = ptx::smem_u32(sB);
-    int ui = 0, sc = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++ui) {
-      const TileMeta t = args.tiles[u / args.mblocks];
+    int sc = 0;
+    for (int j = u_begin; j < u_end; ++j) {
+      const int4 su = __ldg(args.sched + j);
+      const TileMeta t = args.tiles[su.x];
       const uint32_t n_mma = (uint32_t)((t.n_i + 15) & ~15);
       const uint32_t idesc = args.idesc | ((n_mma >> 3) << 17);
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::kAccCols);
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
-      if (lane == 0) trace_evt(args, ui, 2);
+      if (lane == 0) trace_evt(args, j - u_begin, 2);
       for (int kb = 0; kb < t.nkb; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         if (lane == 0) trace_stage(args, sc, 1);
@@ -295,8 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         if (ptx::elect_one()) {
           for (int kk = 0; kk < nk; ++kk) {
             const uint64_t bdesc = ptx::make_sw128_desc(b_base + stage * C::kBBytes + kk * 32, 16, 1024);
-#pragma unroll
-            for (int h = 0; h < C::kHalves; ++h) {
+            for (int h = 0; h < su.z; ++h) {
               const uint64_t adesc =
                   ptx::make_sw128_desc(a_base + stage * C::kABytes + h * 16384 + kk * 2048, 8192, 1024);
               ptx::mma_f16_ss(d_tmem + h * 128, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
@@ -311,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       }
       if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
       __syncwarp();
-      if (lane == 0) trace_evt(args, ui, 3);
+      if (lane == 0) trace_evt(args, j - u_begin, 3);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -321,37 +301,43 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int et = e * 32 + lane;     // 0..255
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     const int h = e >> 2;             // TMEM column half (token half for TB=256, column half for TB=128)
-    const int G = gridDim.x;
     const bool vec = ((args.ldc * (int64_t)sizeof(OutT)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
-    const int64_t row_bytes = (int64_t)args.M * sizeof(OutT);
-    const int64_t unit_bytes = (int64_t)TB * args.avg_cols * sizeof(OutT);
-    int z0 = 0, z1 = 0;
-    if (!args.accumulate && args.n_zero > 0) {
-      z0 = zero_split(args, blockIdx.x, G, total_units, unit_bytes, row_bytes);
-      z1 = max(z0, zero_split(args, blockIdx.x + 1, G, total_units, unit_bytes, row_bytes));
-    }
-    const int my_units = blockIdx.x < total_units ? (total_units - 1 - blockIdx.x) / G + 1 : 0;
+    // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... whenever it
+    // would otherwise wait for an accumulator, and the rest at the end
+    int zr = __ldg(args.zero_off + blockIdx.x) + e;
+    const int z1 = (args.accumulate || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
     constexpr int V = 16 / (int)sizeof(OutT);  // tokens per 16-byte store
     int acc = 0;
     uint32_t acc_phase = 0;
-    int i = 0;
     OutT *out = reinterpret_cast<OutT *>(args.out);
-    for (int u = blockIdx.x; u < total_units; u += G, ++i) {
-      const TileMeta t = args.tiles[u / args.mblocks];
-      const int m0 = (u % args.mblocks) * TB;
+    for (int j = u_begin; j < u_end; ++j) {
+      const int4 su = __ldg(args.sched + j);
+      const TileMeta t = args.tiles[su.x];
+      const int m0 = su.y, nh = su.z;
       if (et < BN) sCol[et] = et < t.n_i ? __ldg(args.colids + t.col_off + et) : -1;
-      // zero part i of my_units (written while unit i's mainloop runs)
-      write_zero_rows<OutT>(args, z0 + (z1 - z0) * i / my_units, z0 + (z1 - z0) * (i + 1) / my_units, e, lane, vec);
-      if (e == 0 && lane == 0) trace_evt(args, i, 4);
-      ptx::mbar_wait(&tfull[acc], acc_phase);
+      if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 4);
+      // wait for the accumulator, writing zero rows meanwhile
+      if (!ptx::mbar_try_wait(&tfull[acc], acc_phase)) {
+        long long t0 = clock64();
+        uint32_t spins = 0;
+        while (!ptx::mbar_try_wait(&tfull[acc], acc_phase)) {
+          if (zr < z1) {
+            write_zero_row<OutT>(args, __ldg(args.zero_rows + zr), lane, vec);
+            zr += kEpiWarps;
+          } else if (((++spins) & 1023u) == 0 && clock64() - t0 > 40000000000LL) {
+            __trap();
+          }
+        }
+      }
       ptx::tc_fence_after();
       epi_sync();  // sCol visible; previous unit's staging reads done
-      if (e == 0 && lane == 0) trace_evt(args, i, 5);
+      if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 5);
       const uint32_t t_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::kAccCols) + h * 128;
       const int n_half0 = min(t.n_i, 128);
+      const int seg = TB == 256 ? nh * 128 : 128;  // tokens per output row segment
       for (int c0 = 0; c0 < n_half0; c0 += 32) {
         // 1) TMEM -> registers -> staging buffer [col][token] (conflict-free)
-        const bool have = TB == 256 ? true : (h * 128 + c0 < t.n_i);
+        const bool have = TB == 256 ? (h < nh) : (h * 128 + c0 < t.n_i);
         if (have) {
           uint32_t v[32];
           ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)c0, v);
@@ -359,10 +345,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
           const int tok = (TB == 256 ? h * 128 : 0) + q * 32 + lane;
           float *dst = sStage + (TB == 256 ? 0 : h * 32 * TB) + tok;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) dst[j * TB] = __uint_as_float(v[j]);
+          for (int jj = 0; jj < 32; ++jj) dst[jj * TB] = __uint_as_float(v[jj]);
         }
         epi_sync();
-        // 2) staged rows -> global, one C^T row segment (TB tokens) at a time
+        // 2) staged rows -> global, one C^T row segment at a time
         constexpr int kRows = C::kStageCols;              // 32 (TB=256) | 64 (TB=128)
         constexpr int kRowsPerWarp = kRows / kEpiWarps;   // 4 | 8
 #pragma unroll 1
@@ -370,10 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
           const int srow = e * kRowsPerWarp + rr;
           const int col = TB == 256 ? c0 + srow : (srow < 32 ? c0 + srow : 128 + c0 + (srow - 32));
           const int orow = col < t.n_i ? sCol[col] : -1;
-          if (orow < 0) continue;
+          if (orow < 0 || (args.debug & 2)) continue;
           OutT *grow = out + (int64_t)orow * args.ldc + m0;
           const float *srow_p = sStage + srow * TB;
-          for (int tk = lane * V; tk < TB; tk += 32 * V) {
+          for (int tk = lane * V; tk < seg; tk += 32 * V) {
             float vals[V];
 #pragma unroll
             for (int x = 0; x < V; x += 4) {
@@ -400,11 +386,11 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
-      if (e == 0 && lane == 0) trace_evt(args, i, 6);
+      if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 6);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (my_units == 0) write_zero_rows<OutT>(args, z0, z1, e, lane, vec);
+    for (; zr < z1; zr += kEpiWarps) write_zero_row<OutT>(args, __ldg(args.zero_rows + zr), lane, vec);
   }
 
   __syncthreads();

@@ -3,10 +3,15 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "tw_b200.h"
+
+#include <vector_types.h>  // int4 (plain header; also fine for host-only TUs)
 
 namespace tw {
 
@@ -16,9 +21,8 @@ void clear_error();
 
 // One live tile of a plan, in launch (LPT) order.  Mirrors a TileTask
 // (engine.py:24-37): the kept-K index list is `kidx[kidx_off .. +nkb*64)`
-// (padded with K, which the TMA gather treats as out of bounds -> zeros),
-// the output rows are `colids[col_off .. +n_i)` (re-based to the plan's
-// column range), the weight image is `wimg + w_off` (nkb blocks of
+// (padded with K), the output rows are `colids[col_off .. +n_i)` (re-based to
+// the plan's column range), the weight image is `wimg + w_off` (nkb blocks of
 // wrows x 128 B, pre-swizzled for the SW128 K-major UMMA operand).
 struct TileMeta {
   int32_t kidx_off;
@@ -36,7 +40,7 @@ struct HostPlan {
   int64_t col_begin = 0, col_end = 0;
   int64_t n_tiles = 0;
   int in_dtype = TW_BF16;
-  int block_n = 128;   // MMA N tile / TMEM columns per accumulator
+  int block_n = 128;   // MMA N tile (<= 256)
   int wrows = 128;     // weight-image rows per k-block (multiple of 16, <= block_n)
   std::vector<TileMeta> tiles;        // live tiles, LPT order
   std::vector<int32_t> src_tile;      // reference tile index of each live tile
@@ -47,6 +51,21 @@ struct HostPlan {
   int64_t kept_elems = 0, union_k = 0, sum_k = 0, sum_n = 0;
 };
 
+// Static work schedule of one launch shape (plan, M, output width): CTA c
+// runs units[off[c] .. off[c+1]) in order -- each {live tile, first token,
+// number of 128-token halves, 0} -- and writes zero rows
+// zero_rows[zoff[c] .. zoff[c+1]) in the gaps.  Built on the host by LPT
+// over a byte-cost model (tw_schedule.cpp).
+struct HostSchedule {
+  int grid = 0;
+  std::vector<int32_t> units;  // 4 ints per unit
+  std::vector<int32_t> off;    // grid + 1
+  std::vector<int32_t> zoff;   // grid + 1
+  double makespan_ns = 0, mean_ns = 0;
+};
+int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows, int sms, int tb,
+                   HostSchedule &s);
+
 // Kernel arguments of the persistent TW-GEMM (tw_gemm_sm100.cu).
 struct GemmArgs {
   const TileMeta *tiles;
@@ -54,20 +73,20 @@ struct GemmArgs {
   const int32_t *colids;
   const int32_t *zero_rows;
   const uint8_t *wimg;
+  const int4 *sched;         // per-CTA unit lists (HostSchedule::units)
+  const int32_t *sched_off;  // grid + 1
+  const int32_t *zero_off;   // grid + 1
   void *out;
   int64_t ldc;
-  const void *at;     // A^T (K x M, 16-bit), row stride lda (cp.async gather path)
+  const void *at;     // A^T (K x M, 16-bit), row stride lda
   int64_t lda;
   int32_t M;
-  int32_t n_live;
-  int32_t mblocks;
-  int32_t n_zero;
   int32_t accumulate;
   int32_t wbytes;     // weight-image bytes per k-block (wrows * 128)
   uint32_t idesc;     // instruction descriptor without the N field
   int32_t block_n;
-  int32_t avg_cols;   // mean live-tile width (zero-row load balancing)
   int64_t *trace;     // optional per-CTA event timeline (tw_gemm_traced), else null
+  int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };
 
 int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,
@@ -80,6 +99,14 @@ uint16_t f32_to_f16_rne(float f);
 
 }  // namespace tw
 
+// Device copy of a schedule, cached per launch shape inside the plan.
+struct tw_dev_schedule {
+  int grid = 0;
+  int4 *units = nullptr;
+  int32_t *off = nullptr;
+  int32_t *zoff = nullptr;
+};
+
 // Device side of a plan (defined in tw_capi.cu).
 struct tw_plan {
   tw::HostPlan host;
@@ -89,4 +116,6 @@ struct tw_plan {
   int32_t *d_colids = nullptr;
   int32_t *d_zero = nullptr;
   uint8_t *d_wimg = nullptr;
+  mutable std::mutex sched_mu;
+  mutable std::map<std::tuple<int64_t, int, int>, tw_dev_schedule> sched;  // (M, out bytes, zero rows on)
 };

@@ -273,6 +273,24 @@ int tw_plan_export(const tw_plan *plan, int which, void *dst, int64_t *bytes) {
   return TW_OK;
 }
 
+int tw_schedule_export(const tw_plan *plan, int64_t m, int out_dtype, int accumulate, int sms, int which, void *dst,
+                       int64_t *bytes) {
+  if (!plan || !bytes) return fail(TW_ERR_ARG, "null pointer");
+  if (m < 1 || sms < 1) return fail(TW_ERR_DIMENSION, "need M >= 1 and sms >= 1");
+  const int tb = plan->host.block_n <= 128 ? 256 : 128;
+  HostSchedule hs;
+  int rc = build_schedule(plan->host, m, out_dtype == TW_F32 ? 4 : 2, !accumulate, sms, tb, hs);
+  if (rc) return rc;
+  const std::vector<int32_t> &v = which == 0 ? hs.units : (which == 1 ? hs.off : hs.zoff);
+  if (which < 0 || which > 2) return fail(TW_ERR_ARG, "bad export selector");
+  const int64_t size = (int64_t)v.size() * 4;
+  if (!dst) { *bytes = size; return TW_OK; }
+  if (*bytes < size) return fail(TW_ERR_ARG, "export buffer too small");
+  if (size) std::memcpy(dst, v.data(), (size_t)size);
+  *bytes = size;
+  return TW_OK;
+}
+
 int tw_plan_get_info(const tw_plan *plan, tw_plan_info *info) {
   if (!plan || !info) return fail(TW_ERR_ARG, "null pointer");
   const HostPlan &hp = plan->host;

@@ -136,6 +136,23 @@ class PackedPlan:
         return out.reshape(-1, 8) if which == "tiles" else out
 
 
+    def schedule(self, m: int, out_dtype: str = "fp32", sms: int = 148, accumulate: bool = False):
+        """The static launch schedule tw_gemm uses for M tokens: per-CTA unit
+        lists ((live tile, first token, 128-token halves) rows) and zero-row
+        ranges.  Host-side; returns (units[n,4], unit_off[G+1], zero_off[G+1])."""
+        code = {"fp32": _lib.TW_F32, "bf16": _lib.TW_BF16, "fp16": _lib.TW_F16}[out_dtype]
+        res = []
+        for which in (0, 1, 2):
+            size = ctypes.c_int64(0)
+            _lib.call("tw_schedule_export", self._h, m, code, int(accumulate), sms, which, None, ctypes.byref(size))
+            buf = np.zeros(max(size.value // 4, 1), np.int32)
+            size2 = ctypes.c_int64(buf.nbytes)
+            _lib.call("tw_schedule_export", self._h, m, code, int(accumulate), sms, which, _np_ptr(buf),
+                      ctypes.byref(size2))
+            res.append(buf[: size.value // 4])
+        return res[0].reshape(-1, 4), res[1], res[2]
+
+
 class TwPlan(PackedPlan):
     """A CompactTileSet packed for the persistent kernel and resident on one
     GPU (see PackedPlan for the layout).

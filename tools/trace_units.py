@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--workload", default="C2a")
     ap.add_argument("--out-dtype", default="fp32")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--cold", action="store_true", help="evict the output from L2 before the traced launch")
     args = ap.parse_args()
     m, k, n, g, s, _ = bench.WORKLOADS[args.workload]
     a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
@@ -50,6 +51,11 @@ def main():
     stream = torch.cuda.current_stream().cuda_stream
     for _ in range(5):
         plan.gemm(at, out=out, out_dtype=dt)
+    if args.cold:  # push this launch's output out of L2 first (as in bench.py's rotation)
+        others = [torch.empty_like(out) for _ in range(5)]
+        ats = [at.clone() for _ in range(5)]
+        for o, a2 in zip(others, ats):
+            plan.gemm(a2, out=o, out_dtype=dt)
     torch.cuda.synchronize()
     trace.zero_()
     _lib.call("tw_gemm_traced", plan._h, at.data_ptr(), m, at.stride(0), out.data_ptr(), out.stride(0), code,
