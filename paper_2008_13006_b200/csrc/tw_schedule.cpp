@@ -144,17 +144,22 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
     if (full < base.size() && full > 0) cands.push_back(split(full));
     cands.push_back(split(0));
   }
-  double best = 1e300;
+  // Pick the candidate with the shortest unit-only makespan (a CTA's units
+  // run back to back and their outputs cannot be written before their MMA
+  // completes); the zero rows are then water-filled around it.
+  double best = 1e300, best_total = 0;
   size_t best_i = 0;
   std::vector<int> best_owner;
   std::vector<int64_t> best_z;
   for (size_t ci = 0; ci < cands.size(); ++ci) {
     std::vector<int> owner;
     std::vector<double> load = lpt(cands[ci], G, &owner);
+    const double unit_mk = *std::max_element(load.begin(), load.end());
     double mk = 0;
     std::vector<int64_t> z = water_fill(load, Z, zc, &mk);
-    if (mk < best * 0.999) {
-      best = mk;
+    if (unit_mk < best * 0.98 || (unit_mk < best * 1.02 && mk < best_total)) {
+      best = unit_mk;
+      best_total = mk;
       best_i = ci;
       best_owner = owner;
       best_z = z;
@@ -178,7 +183,7 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
     s.zoff[(size_t)c + 1] = (int32_t)(s.zoff[(size_t)c] + (best_z.empty() ? 0 : best_z[(size_t)c]));
   }
   if (s.zoff[(size_t)G] != Z) return fail(TW_ERR_ARG, "internal: zero-row schedule does not cover the zero list");
-  s.makespan_ns = best;
+  s.makespan_ns = best_total;
   s.mean_ns = (total + Z * zc) / G;
   return TW_OK;
 }
