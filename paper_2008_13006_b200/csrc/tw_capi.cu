@@ -54,6 +54,12 @@ int require_sm100(int *sms) {
   if (rc) return rc;
   if (major != 10) return fail(TW_ERR_CUDA, "libtw_b200 requires an sm_100 (B200) device; found compute capability " +
                                                 std::to_string(major) + ".x");
+  // experiment knob: schedule for fewer SMs (profiling only)
+  static const int cap = [] {
+    const char *e = std::getenv("TW_B200_SMS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (cap > 0 && cap < *sms) *sms = cap;
   return TW_OK;
 }
 

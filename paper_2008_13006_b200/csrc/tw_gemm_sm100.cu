@@ -58,13 +58,13 @@ struct Cfg {
   static constexpr int kHalves = TB / 128;                    // max M=128 MMAs per k-step
   static constexpr uint32_t kABytes = TB * kBlockK * 2;       // 32 KB | 16 KB
   static constexpr uint32_t kBBytes = BN * 128;               // 16 KB | 32 KB
-  static constexpr int kStages = 4;
+  static constexpr int kStages = 3;
   static constexpr uint32_t kAccCols = 256;                   // TMEM columns per accumulator
   static constexpr uint32_t kTmemCols = 2 * kAccCols;
   static constexpr int kStageCols = kHalves == 2 ? 32 : 64;   // staged C^T rows per chunk
-  static constexpr uint32_t kStageBytes = 32768;              // chunk staging buffer (fp32)
+  static constexpr uint32_t kStageBytes = 32768;              // one chunk staging buffer (fp32); two are used
   static constexpr uint32_t kSmem =
-      1024 /*align slack*/ + kStages * (kABytes + kBBytes) + kStageBytes + 1024 /*col ids*/ + 256 /*barriers*/;
+      1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 2 * kStageBytes + 1024 /*col ids*/ + 256 /*barriers*/;
 };
 
 template <typename T>
@@ -153,6 +153,15 @@ __device__ __forceinline__ void trace_stage(const GemmArgs &a, int s, int slot) 
   }
 }
 
+// epilogue chunk events of each CTA's first unit (after the stage table)
+__device__ __forceinline__ void trace_epi(const GemmArgs &a, int idx) {
+  if (a.trace != nullptr && idx < 32) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[(int64_t)gridDim.x * 192 + (int64_t)blockIdx.x * 32 + idx] = (int64_t)t;
+  }
+}
+
 template <int BN, typename OutT>
 __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid_constant__ GemmArgs args) {
   using C = Cfg<BN>;
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::kStages * C::kABytes;
   float *sStage = reinterpret_cast<float *>(sB + C::kStages * C::kBBytes);
-  int32_t *sCol = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(sStage) + C::kStageBytes);
+  int32_t *sCol = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(sStage) + 2 * C::kStageBytes);
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sCol) + 1024);
   uint64_t *empty = full + C::kStages;
   uint64_t *tfull = empty + C::kStages;
@@ -334,20 +343,35 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 5);
       const uint32_t t_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::kAccCols) + h * 128;
       const int n_half0 = min(t.n_i, 128);
+      const int n_chunks = (n_half0 + 31) / 32;
       const int seg = TB == 256 ? nh * 128 : 128;  // tokens per output row segment
-      for (int c0 = 0; c0 < n_half0; c0 += 32) {
+      for (int ci = 0; ci < n_chunks; ++ci) {
+        const int c0 = ci * 32;
+        float *buf = sStage + (ci & 1) * (C::kStageBytes / 4);  // double-buffered staging
         // 1) TMEM -> registers -> staging buffer [col][token] (conflict-free)
         const bool have = TB == 256 ? (h < nh) : (h * 128 + c0 < t.n_i);
         if (have) {
           uint32_t v[32];
           ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)c0, v);
           ptx::tmem_ld_wait();
+          if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 0);
           const int tok = (TB == 256 ? h * 128 : 0) + q * 32 + lane;
-          float *dst = sStage + (TB == 256 ? 0 : h * 32 * TB) + tok;
+          float *dst = buf + (TB == 256 ? 0 : h * 32 * TB) + tok;
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) dst[jj * TB] = __uint_as_float(v[jj]);
         }
+        if (ci == n_chunks - 1) {
+          // all of this warp's TMEM reads for the unit are done: hand the
+          // accumulator back to the MMA warp before storing the last chunk
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&tempty[acc]);
+        }
+        if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 1);
+        // One barrier per chunk: it publishes buf[ci & 1] and (double
+        // buffering) guarantees every warp finished storing chunk ci - 1,
+        // whose buffer chunk ci + 1 will overwrite.
         epi_sync();
+        if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 2);
         // 2) staged rows -> global, one C^T row segment at a time
         constexpr int kRows = C::kStageCols;              // 32 (TB=256) | 64 (TB=128)
         constexpr int kRowsPerWarp = kRows / kEpiWarps;   // 4 | 8
@@ -358,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
           const int orow = col < t.n_i ? sCol[col] : -1;
           if (orow < 0 || (args.debug & 2)) continue;
           OutT *grow = out + (int64_t)orow * args.ldc + m0;
-          const float *srow_p = sStage + srow * TB;
+          const float *srow_p = buf + srow * TB;
           for (int tk = lane * V; tk < seg; tk += 32 * V) {
             float vals[V];
 #pragma unroll
@@ -382,10 +406,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
             }
           }
         }
-        epi_sync();  // staging buffer free for the next chunk
+        if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 3);
       }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 6);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;

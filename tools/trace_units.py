@@ -46,24 +46,26 @@ def main():
     out = torch.empty((n, m), dtype=dt, device="cuda")
     sms = ctypes.c_int(0)
     _lib.call("tw_device_sm_count", ctypes.byref(sms))
-    trace = torch.zeros(sms.value * (64 + 128), dtype=torch.int64, device="cuda")
+    trace = torch.zeros(sms.value * (64 + 128 + 32), dtype=torch.int64, device="cuda")
     code = {"fp32": 0, "bf16": 1, "fp16": 2}[args.out_dtype]
     stream = torch.cuda.current_stream().cuda_stream
     for _ in range(5):
         plan.gemm(at, out=out, out_dtype=dt)
-    if args.cold:  # push this launch's output out of L2 first (as in bench.py's rotation)
-        others = [torch.empty_like(out) for _ in range(5)]
-        ats = [at.clone() for _ in range(5)]
-        for o, a2 in zip(others, ats):
-            plan.gemm(a2, out=o, out_dtype=dt)
+    others = [torch.empty_like(out) for _ in range(5)] if args.cold else []
+    ats = [at.clone() for _ in range(5)] if args.cold else []
     torch.cuda.synchronize()
     trace.zero_()
+    # --cold: back-to-back launches on rotating buffers right before the traced
+    # one, with no sync in between (bench.py's steady state)
+    for o, a2 in zip(others, ats):
+        plan.gemm(a2, out=o, out_dtype=dt)
     _lib.call("tw_gemm_traced", plan._h, at.data_ptr(), m, at.stride(0), out.data_ptr(), out.stride(0), code,
               trace.data_ptr(), stream)
     torch.cuda.synchronize()
     full = trace.cpu().numpy().astype(np.float64)
     tr = full[: sms.value * 64].reshape(sms.value, 8, 8)
-    st = full[sms.value * 64:].reshape(sms.value, 32, 4)
+    st = full[sms.value * 64: sms.value * 192].reshape(sms.value, 32, 4)
+    ep = full[sms.value * 192:].reshape(sms.value, 32)
     valid = tr > 0
     t0 = tr[valid].min()
     rel = np.where(valid, (tr - t0) / 1e3, np.nan)  # us
@@ -82,6 +84,11 @@ def main():
         c0 = srel[0, si]
         print(f"{si:5d} {np.nanmedian(srel[:, si, 0]):9.2f} {np.nanmedian(srel[:, si, 1]):9.2f} "
               f"{np.nanmedian(srel[:, si, 2]):9.2f}     [{c0[0]:7.2f} {c0[1]:7.2f} {c0[2]:7.2f}]")
+    erel = np.where(ep > 0, (ep - t0) / 1e3, np.nan)
+    print("epilogue chunk c of unit 0 (median over CTAs): ld_done sts_done synced stored")
+    for c in range(8):
+        row = [np.nanmedian(erel[:, c * 4 + x]) if np.isfinite(erel[:, c * 4 + x]).any() else float("nan") for x in range(4)]
+        print(f"  chunk {c}: " + " ".join(f"{v:7.2f}" for v in row))
     # per-unit durations
     mma = rel[:, :, 3] - rel[:, :, 2]
     prod = rel[:, :, 1] - rel[:, :, 0]
