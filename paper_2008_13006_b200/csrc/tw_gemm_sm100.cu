@@ -64,7 +64,7 @@ struct Cfg {
   static constexpr int kStageCols = kHalves == 2 ? 32 : 64;   // staged C^T rows per chunk
   static constexpr uint32_t kStageBytes = 32768;              // one chunk staging buffer (fp32); two are used
   static constexpr uint32_t kSmem =
-      1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 2 * kStageBytes + 1024 /*col ids*/ + 256 /*barriers*/;
+      1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 2 * kStageBytes + 2048 /*col ids x2*/ + 256 /*barriers*/;
 };
 
 template <typename T>
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   uint8_t *sB = smem + C::kStages * C::kABytes;
   float *sStage = reinterpret_cast<float *>(sB + C::kStages * C::kBBytes);
   int32_t *sCol = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(sStage) + 2 * C::kStageBytes);
-  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sCol) + 1024);
+  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sCol) + 2048);
   uint64_t *empty = full + C::kStages;
   uint64_t *tfull = empty + C::kStages;
   uint64_t *tempty = tfull + 2;
@@ -323,7 +323,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       const int4 su = __ldg(args.sched + j);
       const TileMeta t = args.tiles[su.x];
       const int m0 = su.y, nh = su.z;
-      if (et < BN) sCol[et] = et < t.n_i ? __ldg(args.colids + t.col_off + et) : -1;
+      // col ids double-buffered by unit parity: a fast warp may fill the next
+      // unit's table while others still store this unit's last chunk
+      int32_t *ucol = sCol + ((j - u_begin) & 1) * 256;
+      if (et < BN) ucol[et] = et < t.n_i ? __ldg(args.colids + t.col_off + et) : -1;
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 4);
       // wait for the accumulator, writing zero rows meanwhile
       if (!ptx::mbar_try_wait(&tfull[acc], acc_phase)) {
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         for (int rr = 0; rr < kRowsPerWarp; ++rr) {
           const int srow = e * kRowsPerWarp + rr;
           const int col = TB == 256 ? c0 + srow : (srow < 32 ? c0 + srow : 128 + c0 + (srow - 32));
-          const int orow = col < t.n_i ? sCol[col] : -1;
+          const int orow = col < t.n_i ? ucol[col] : -1;
           if (orow < 0 || (args.debug & 2)) continue;
           OutT *grow = out + (int64_t)orow * args.ldc + m0;
           const float *srow_p = buf + srow * TB;
