@@ -63,8 +63,9 @@ struct Cfg {
   static constexpr uint32_t kTmemCols = 2 * kAccCols;
   static constexpr int kStageCols = kHalves == 2 ? 32 : 64;   // staged C^T rows per chunk
   static constexpr uint32_t kStageBytes = 32768;              // one chunk staging buffer (fp32); two are used
+  static constexpr uint32_t kZeroBytes = 8192;              // zero source for TMA bulk zero-row stores
   static constexpr uint32_t kSmem =
-      1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 2 * kStageBytes + 2048 /*col ids x2*/ + 256 /*barriers*/;
+      1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 2 * kStageBytes + kZeroBytes + 2048 /*col ids x2*/ + 256 /*barriers*/;
 };
 
 template <typename T>
@@ -133,6 +134,29 @@ __device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int l
   for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(0.f);
 }
 
+// One zero row by TMA bulk stores from a zeroed shared buffer (issued by one
+// lane; no LSU traffic, 8 KB per request).  Falls back to STG when the row is
+// not 16-byte aligned / sized.
+template <typename OutT>
+__device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int lane, bool bulk_ok, bool vec,
+                                              const uint8_t *zero_buf, uint32_t zero_bytes) {
+  if (!bulk_ok) {
+    write_zero_row<OutT>(a, row, lane, vec);
+    return;
+  }
+  if (lane == 0) {
+    char *dst = reinterpret_cast<char *>(a.out) + (int64_t)row * a.ldc * (int64_t)sizeof(OutT);
+    const int64_t bytes = (int64_t)a.M * (int64_t)sizeof(OutT);
+    for (int64_t off = 0; off < bytes; off += zero_bytes) {
+      const uint32_t n = (uint32_t)min((int64_t)zero_bytes, bytes - off);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + off),
+                   "r"(ptx::smem_u32(zero_buf)), "r"(n)
+                   : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
 // committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
@@ -154,11 +178,10 @@ __device__ __forceinline__ void trace_stage(const GemmArgs &a, int s, int slot) 
 }
 
 // epilogue chunk events of each CTA's first unit (after the stage table)
+// (SM clock cycles, not globaltimer: the intervals are sub-microsecond)
 __device__ __forceinline__ void trace_epi(const GemmArgs &a, int idx) {
   if (a.trace != nullptr && idx < 32) {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[(int64_t)gridDim.x * 192 + (int64_t)blockIdx.x * 32 + idx] = (int64_t)t;
+    a.trace[(int64_t)gridDim.x * 192 + (int64_t)blockIdx.x * 32 + idx] = (int64_t)clock64();
   }
 }
 
@@ -171,7 +194,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::kStages * C::kABytes;
   float *sStage = reinterpret_cast<float *>(sB + C::kStages * C::kBBytes);
-  int32_t *sCol = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(sStage) + 2 * C::kStageBytes);
+  uint8_t *sZero = reinterpret_cast<uint8_t *>(sStage) + 2 * C::kStageBytes;
+  int32_t *sCol = reinterpret_cast<int32_t *>(sZero + C::kZeroBytes);
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sCol) + 2048);
   uint64_t *empty = full + C::kStages;
   uint64_t *tfull = empty + C::kStages;
@@ -182,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   const int lane = threadIdx.x & 31;
   const int u_begin = __ldg(args.sched_off + blockIdx.x);
   const int u_end = __ldg(args.sched_off + blockIdx.x + 1);
+  if (threadIdx.x == 0) trace_evt(args, 7, 0);  // CTA start
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -194,6 +219,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     }
     ptx::fence_mbar_init();
   }
+  for (int i = threadIdx.x; i < (int)(C::kZeroBytes / 16); i += kThreads)
+    reinterpret_cast<uint4 *>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  ptx::fence_proxy_async_smem();  // the zero buffer is read by the TMA (async proxy)
   if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
@@ -279,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       for (int kb = 0; kb < t.nkb; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         if (lane == 0) trace_stage(args, sc, 1);
-        ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
+        if (!(args.debug & 8)) ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
         ptx::tc_fence_after();
         const int nk = min(4, t.k16 - kb * 4);
         if (ptx::elect_one()) {
@@ -288,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
             for (int h = 0; h < su.z; ++h) {
               const uint64_t adesc =
                   ptx::make_sw128_desc(a_base + stage * C::kABytes + h * 16384 + kk * 2048, 8192, 1024);
-              ptx::mma_f16_ss(d_tmem + h * 128, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
+              if (!(args.debug & 4)) ptx::mma_f16_ss(d_tmem + h * 128, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
             }
           }
           ptx::mma_commit(&empty[stage]);
@@ -311,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     const int h = e >> 2;             // TMEM column half (token half for TB=256, column half for TB=128)
     const bool vec = ((args.ldc * (int64_t)sizeof(OutT)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
+    const bool bulk_ok = vec && ((int64_t)args.M * (int64_t)sizeof(OutT)) % 16 == 0;
     // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... whenever it
     // would otherwise wait for an accumulator, and the rest at the end
     int zr = __ldg(args.zero_off + blockIdx.x) + e;
@@ -329,18 +358,13 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (et < BN) ucol[et] = et < t.n_i ? __ldg(args.colids + t.col_off + et) : -1;
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 4);
       // wait for the accumulator, writing zero rows meanwhile
-      if (!ptx::mbar_try_wait(&tfull[acc], acc_phase)) {
-        long long t0 = clock64();
-        uint32_t spins = 0;
-        while (!ptx::mbar_try_wait(&tfull[acc], acc_phase)) {
-          if (zr < z1) {
-            write_zero_row<OutT>(args, __ldg(args.zero_rows + zr), lane, vec);
-            zr += kEpiWarps;
-          } else if (((++spins) & 1023u) == 0 && clock64() - t0 > 40000000000LL) {
-            __trap();
-          }
-        }
+      // (non-blocking test_wait while there is filler work: try_wait would
+      // suspend the warp for up to its time limit between zero rows)
+      while (zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
+        zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok && (args.debug & 32), vec, sZero, C::kZeroBytes);
+        zr += kEpiWarps;
       }
+      ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       epi_sync();  // sCol visible; previous unit's staging reads done
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 5);
@@ -378,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         // 2) staged rows -> global, one C^T row segment at a time
         constexpr int kRows = C::kStageCols;              // 32 (TB=256) | 64 (TB=128)
         constexpr int kRowsPerWarp = kRows / kEpiWarps;   // 4 | 8
-#pragma unroll 1
+#pragma unroll
         for (int rr = 0; rr < kRowsPerWarp; ++rr) {
           const int srow = e * kRowsPerWarp + rr;
           const int col = TB == 256 ? c0 + srow : (srow < 32 ? c0 + srow : 128 + c0 + (srow - 32));
@@ -396,7 +420,12 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
             if (vec && m0 + tk + V <= args.M) {
               uint4 *p = reinterpret_cast<uint4 *>(grow + tk);
               if (args.accumulate) unpack16_add<OutT>(*p, vals);
-              __stcs(p, pack16<OutT>(vals));
+              const uint4 pk = pack16<OutT>(vals);
+              if (args.debug & 16) {  // experiment: staging reads without the global store
+                if ((pk.x ^ pk.y ^ pk.z ^ pk.w) == 0x7fc00001u) __stcs(p, pk);
+              } else {
+                __stcs(p, pk);
+              }
             } else {
 #pragma unroll
               for (int x = 0; x < V; ++x) {
@@ -415,7 +444,11 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    for (; zr < z1; zr += kEpiWarps) write_zero_row<OutT>(args, __ldg(args.zero_rows + zr), lane, vec);
+    for (; zr < z1; zr += kEpiWarps)
+      zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok && (args.debug & 32), vec, sZero, C::kZeroBytes);
+    if (e == 0 && lane == 0) trace_evt(args, 7, 1);  // last zero row issued
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // bulk stores done before exit
+    if (e == 0 && lane == 0) trace_evt(args, 7, 2);  // bulk stores drained
   }
 
   __syncthreads();

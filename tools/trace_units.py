@@ -84,11 +84,16 @@ def main():
         c0 = srel[0, si]
         print(f"{si:5d} {np.nanmedian(srel[:, si, 0]):9.2f} {np.nanmedian(srel[:, si, 1]):9.2f} "
               f"{np.nanmedian(srel[:, si, 2]):9.2f}     [{c0[0]:7.2f} {c0[1]:7.2f} {c0[2]:7.2f}]")
-    erel = np.where(ep > 0, (ep - t0) / 1e3, np.nan)
-    print("epilogue chunk c of unit 0 (median over CTAs): ld_done sts_done synced stored")
+    base = np.where(ep[:, :1] > 0, ep[:, :1], np.nan)
+    erel = np.where(ep > 0, ep - base, np.nan)  # SM cycles since chunk 0's TMEM load completed
+    print("epilogue chunk c of unit 0 (median over CTAs, SM cycles from chunk-0 ld): ld_done sts_done synced stored")
     for c in range(8):
         row = [np.nanmedian(erel[:, c * 4 + x]) if np.isfinite(erel[:, c * 4 + x]).any() else float("nan") for x in range(4)]
-        print(f"  chunk {c}: " + " ".join(f"{v:7.2f}" for v in row))
+        print(f"  chunk {c}: " + " ".join(f"{v:8.0f}" for v in row))
+    ends = rel[:, 7, :3]
+    print("CTA start / zeros issued / drained (min med max):",
+          [(round(float(np.nanmin(ends[:, i])), 2), round(float(np.nanmedian(ends[:, i])), 2),
+            round(float(np.nanmax(ends[:, i])), 2)) for i in range(3)])
     # per-unit durations
     mma = rel[:, :, 3] - rel[:, :, 2]
     prod = rel[:, :, 1] - rel[:, :, 0]
