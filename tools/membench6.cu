@@ -98,6 +98,43 @@ __global__ void gather_tma_store(const __nv_bfloat16 *at, int stages, char *out,
   }
 }
 
+// gather (4 warps) with 9 more warps parked on an mbarrier try_wait loop
+// (as the kernel's MMA / epilogue warps are) -- do they slow the gathers?
+template <int kDepth>
+__global__ void gather_spinners(const __nv_bfloat16 *at, int stages, long long *cyc) {
+  extern __shared__ __align__(1024) char sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bar)));
+  }
+  __syncthreads();
+  if (warp < 4) {
+    long long t0 = clock64();
+    for (int i = 0; i < stages; ++i) {
+      for (int it = 0; it < 16; ++it) {
+        const int r = warp * 16 + it;
+        const int krow = (r * 389 + i * 13 + blockIdx.x * 7) % 768;
+        cp16(sm + (i % kDepth) * 32768 + r * 512 + lane * 16,
+             at + (int64_t)krow * 4096 + ((blockIdx.x * 256 + i * 256) % 4096) + lane * 8);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(kDepth - 1) : "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (threadIdx.x == 0) {
+      cyc[blockIdx.x] = clock64() - t0;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(&bar)));
+    }
+  } else {
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.b32 %0,1,0,p;\n\t}"
+                   : "=r"(ok)
+                   : "r"((uint32_t)__cvta_generic_to_shared(&bar)));
+  }
+}
+
 template <int D, bool S>
 void run(const __nv_bfloat16 *at, float4 *out, long long *cyc, int sms) {
   auto k = gather<D, S>;
@@ -149,6 +186,21 @@ int main() {
     for (int i = 0; i < sms; ++i) avg += h[i];
     avg /= sms;
     printf("gathers + TMA bulk stores on the same SM: %6.1f B/clk/SM (~%5.1f GB/s/SM)\n", 64.0 * 32768 / avg,
+           64.0 * 32768 / avg * 1.9);
+  }
+  {
+    auto k = gather_spinners<3>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32768);
+    for (int r = 0; r < 2; ++r) {
+      k<<<sms, 416, 3 * 32768>>>(at, 64, cyc);
+      cudaDeviceSynchronize();
+    }
+    long long h[256];
+    cudaMemcpy(h, cyc, sms * 8, cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < sms; ++i) avg += h[i];
+    avg /= sms;
+    printf("gather depth 3 + 9 spinning warps: %6.1f B/clk/SM (~%5.1f GB/s/SM)\n", 64.0 * 32768 / avg,
            64.0 * 32768 / avg * 1.9);
   }
   // split roles: even CTAs gather only, odd CTAs store only

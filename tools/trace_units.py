@@ -35,13 +35,18 @@ def main():
     ap.add_argument("--workload", default="C2a")
     ap.add_argument("--out-dtype", default="fp32")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--pad", type=int, default=0, help="extra elements per A^T row (row pitch)")
     ap.add_argument("--cold", action="store_true", help="evict the output from L2 before the traced launch")
     args = ap.parse_args()
     m, k, n, g, s, _ = bench.WORKLOADS[args.workload]
     a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
     ts = tw.compact(tw.DenseMatrix.from_array(w), bench.to_pattern(tw, p))
     plan = tw.TwPlan(ts)
-    at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
+    if args.pad:
+        buf = torch.empty((k, m + args.pad), dtype=torch.bfloat16, device="cuda")[:, :m]
+        at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16, out=buf)
+    else:
+        at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
     dt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[args.out_dtype]
     out = torch.empty((n, m), dtype=dt, device="cuda")
     sms = ctypes.c_int(0)
