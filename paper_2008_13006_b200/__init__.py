@@ -34,6 +34,7 @@ from .pattern import (
     unpack_mask_words,
     zero_fill,
 )
+from .sharded import ShardedTwPlan, all_gather_rows, shard_ranges
 from .engine import (
     DeviceCsc,
     FlopReport,
