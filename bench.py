@@ -297,7 +297,7 @@ def run_ours(args):
     # ---- timed region (device events), clocks sampled during soak + timing
     barrier()
     with ClockSampler(local) as clk:
-        ms = time_device(torch, step, args.steps, args.warmup, soak_s=args.soak)
+        ms = time_device(torch, step, args.steps, max(args.warmup, n_sets), soak_s=args.soak)
     barrier()
     ms_all = ms
     if pg is not None:
@@ -319,7 +319,7 @@ def run_ours(args):
     result = {}
     if rank == 0:
         # same steps launched eagerly from Python (per-call host overhead visible)
-        result["eager_ms"] = time_device(torch, step, args.steps, 3, graph=False)
+        result["eager_ms"] = time_device(torch, step, args.steps, n_sets, graph=False)
         # ---- other output dtypes (same kernel, 16-bit epilogue)
         variants = {}
         for name, dt, ob in (("fp16_out", torch.float16, 2), ("bf16_out", torch.bfloat16, 2), ("fp32_out", torch.float32, 4)):
@@ -327,7 +327,7 @@ def run_ours(args):
                 continue
             vo = [torch.empty((n_layer, m), dtype=dt, device=dev) for _ in range(n_sets)]
             vms = time_device(torch, lambda i: plans[i % n_sets].gemm(ats[i % n_sets], out=vo[i % n_sets], out_dtype=dt),
-                              args.steps, args.warmup)
+                              args.steps, max(args.warmup, n_sets))
             b = algorithmic_bytes(info, m, ob)
             variants[name] = {"ms_per_step": vms, "tflops_dense_equiv": dense_flops / (vms * 1e-3) / 1e12,
                               "hbm_gbs": b / (vms * 1e-3) / 1e9, "hbm_frac": b / (vms * 1e-3) / 1e9 / hbm_peak}
@@ -339,11 +339,11 @@ def run_ours(args):
         w_sets = [w_bf] + [w_bf.clone() for _ in range(n_sets - 1)]
         c16 = [torch.empty((m, n_layer), dtype=torch.bfloat16, device=dev) for _ in range(n_sets)]
         cub16 = time_device(torch, lambda i: torch.mm(a_sets[i % n_sets], w_sets[i % n_sets], out=c16[i % n_sets]),
-                            args.steps, args.warmup)
+                            args.steps, max(args.warmup, n_sets))
         del c16
         c32 = [torch.empty((m, n_layer), dtype=torch.float32, device=dev) for _ in range(n_sets)]
         cub32 = time_device(torch, lambda i: torch.mm(a_sets[i % n_sets], w_sets[i % n_sets], out_dtype=torch.float32,
-                                                      out=c32[i % n_sets]), args.steps, args.warmup)
+                                                      out=c32[i % n_sets]), args.steps, max(args.warmup, n_sets))
         del c32, a_sets, w_sets
         result.update(cublas={"bf16_out_ms": cub16, "fp32_out_ms": cub32,
                               "bf16_out_tflops": dense_flops / (cub16 * 1e-3) / 1e12,

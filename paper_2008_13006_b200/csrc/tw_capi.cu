@@ -76,6 +76,15 @@ int upload(T **dst, const std::vector<T> &src) {
 
 int out_size(int dtype) { return dtype == TW_F32 ? 4 : 2; }
 
+void free_schedule(tw_dev_schedule &ds) {
+  cudaFree(ds.units);
+  cudaFree(ds.off);
+  cudaFree(ds.zoff);
+  cudaFree(ds.stream);
+  cudaFree(ds.soff);
+  ds = tw_dev_schedule{};
+}
+
 // Static schedule for (M, output width, zero rows on/off), built once per
 // launch shape and cached on the plan (uploaded to the plan's device).
 int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, const tw_dev_schedule **out) {
@@ -95,10 +104,10 @@ int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, c
   std::vector<int4> units(hs.units.size() / 4);
   for (size_t i = 0; i < units.size(); ++i)
     units[i] = make_int4(hs.units[4 * i], hs.units[4 * i + 1], hs.units[4 * i + 2], hs.units[4 * i + 3]);
-  if ((rc = upload(&ds.units, units)) || (rc = upload(&ds.off, hs.off)) || (rc = upload(&ds.zoff, hs.zoff))) {
-    cudaFree(ds.units);
-    cudaFree(ds.off);
-    cudaFree(ds.zoff);
+  if (hs.stream.empty()) hs.stream.assign(68, -1);
+  if ((rc = upload(&ds.units, units)) || (rc = upload(&ds.off, hs.off)) || (rc = upload(&ds.zoff, hs.zoff)) ||
+      (rc = upload(&ds.stream, hs.stream)) || (rc = upload(&ds.soff, hs.soff))) {
+    free_schedule(ds);
     return rc;
   }
   auto ins = p->sched.emplace(key, ds);
@@ -167,11 +176,7 @@ int tw_plan_destroy(tw_plan *p) {
   cudaFree(p->d_colids);
   cudaFree(p->d_zero);
   cudaFree(p->d_wimg);
-  for (auto &kv : p->sched) {
-    cudaFree(kv.second.units);
-    cudaFree(kv.second.off);
-    cudaFree(kv.second.zoff);
-  }
+  for (auto &kv : p->sched) free_schedule(kv.second);
   if (prev != p->device) cudaSetDevice(prev);
   delete p;
   return TW_OK;
@@ -226,6 +231,8 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.sched = sched->units;
   a.sched_off = sched->off;
   a.zero_off = sched->zoff;
+  a.stream = sched->stream;
+  a.stream_off = sched->soff;
   a.out = ct;
   a.ldc = ldc;
   a.at = at;
@@ -239,6 +246,11 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 15) | ((128u >> 4) << 24);
   a.block_n = hp.block_n;
   a.trace = trace;
+  static const int zero_policy = [] {
+    const char *e = std::getenv("TW_B200_ZERO");
+    return e ? std::atoi(e) : 1;
+  }();
+  a.zero_policy = zero_policy;
   if (trace) {  // experiment knobs only honoured on the profiling entry point
     const char *dbg = std::getenv("TW_B200_DEBUG");
     a.debug = dbg ? std::atoi(dbg) : 0;

@@ -51,6 +51,14 @@ constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreads = (kProducerWarps + 1 + kEpiWarps) * 32;
 constexpr int kBlockK = 64;
 constexpr int kEpiBarrier = 1;  // named barrier id for the epilogue warps
+// Per-CTA stage stream (HostSchedule::stream): 64 kept-row indices + a
+// 4-int record per 64-k stage.  Each producer warp prefetches its 16 indices
+// and the record of stage i + kIdxLook into its own shared-memory ring with
+// cp.async while issuing stage i: no register ever waits on an index load.
+constexpr int kIdxInts = 68;
+constexpr int kSlotInts = 20;  // 16 row indices + the 4-int record
+constexpr int kIdxSlots = 8;
+constexpr int kIdxLook = 4;
 
 template <int BN>
 struct Cfg {
@@ -58,14 +66,22 @@ struct Cfg {
   static constexpr int kHalves = TB / 128;                    // max M=128 MMAs per k-step
   static constexpr uint32_t kABytes = TB * kBlockK * 2;       // 32 KB | 16 KB
   static constexpr uint32_t kBBytes = BN * 128;               // 16 KB | 32 KB
-  static constexpr int kStages = 3;
   static constexpr uint32_t kAccCols = 256;                   // TMEM columns per accumulator
   static constexpr uint32_t kTmemCols = 2 * kAccCols;
-  static constexpr int kStageCols = kHalves == 2 ? 32 : 64;   // staged C^T rows per chunk
-  static constexpr uint32_t kStageBytes = 32768;              // one chunk staging buffer (fp32); two are used
-  static constexpr uint32_t kZeroBytes = 8192;              // zero source for TMA bulk zero-row stores
-  static constexpr uint32_t kSmem =
-      1024 /*align slack*/ + kStages * (kABytes + kBBytes) + 2 * kStageBytes + kZeroBytes + 2048 /*col ids x2*/ + 256 /*barriers*/;
+  static constexpr int kChunk = 16;                           // accumulator columns per epilogue chunk
+  static constexpr int kStageCols = kHalves == 2 ? kChunk : 2 * kChunk;  // staged C^T rows per chunk
+  static constexpr uint32_t kStageBytes = kStageCols * TB * 4;          // 16 KB; two are used
+  static constexpr uint32_t kColBytes = 2 * BN * 4;                     // col-id table, double buffered
+  static constexpr uint32_t kFixed =
+      1024 /*align slack*/ + 2 * kStageBytes + kColBytes + 256 /*barriers*/ + kProducerWarps * kIdxSlots * kSlotInts * 4;
+  // as many 64-k pipeline stages as fit next to the epilogue buffers (4 for
+  // G <= 128): bytes in flight per SM set the gather throughput
+  static constexpr int kStages = (int)((232448u - kFixed) / (kABytes + kBBytes)) > 4
+                                     ? 4
+                                     : (int)((232448u - kFixed) / (kABytes + kBBytes));
+  static constexpr uint32_t kSmem = kFixed + kStages * (kABytes + kBBytes);
+  static_assert(kStages >= 3, "pipeline too shallow");
+  static_assert(kSmem <= 232448u, "shared memory budget");
 };
 
 template <typename T>
@@ -134,29 +150,6 @@ __device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int l
   for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(0.f);
 }
 
-// One zero row by TMA bulk stores from a zeroed shared buffer (issued by one
-// lane; no LSU traffic, 8 KB per request).  Falls back to STG when the row is
-// not 16-byte aligned / sized.
-template <typename OutT>
-__device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int lane, bool bulk_ok, bool vec,
-                                              const uint8_t *zero_buf, uint32_t zero_bytes) {
-  if (!bulk_ok) {
-    write_zero_row<OutT>(a, row, lane, vec);
-    return;
-  }
-  if (lane == 0) {
-    char *dst = reinterpret_cast<char *>(a.out) + (int64_t)row * a.ldc * (int64_t)sizeof(OutT);
-    const int64_t bytes = (int64_t)a.M * (int64_t)sizeof(OutT);
-    for (int64_t off = 0; off < bytes; off += zero_bytes) {
-      const uint32_t n = (uint32_t)min((int64_t)zero_bytes, bytes - off);
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + off),
-                   "r"(ptx::smem_u32(zero_buf)), "r"(n)
-                   : "memory");
-    }
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
-}
-
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
 // committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
@@ -189,23 +182,30 @@ template <int BN, typename OutT>
 __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid_constant__ GemmArgs args) {
   using C = Cfg<BN>;
   constexpr int TB = C::TB;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1 KB alignment (SW128 atoms) by pointer arithmetic on the __shared__
+  // array, NOT through an integer cast: the compiler must keep seeing a
+  // shared-space pointer, or every access below becomes a generic LD/ST that
+  // queues in the LSU behind this SM's outstanding gathers and stores.
+  uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::kStages * C::kABytes;
   float *sStage = reinterpret_cast<float *>(sB + C::kStages * C::kBBytes);
-  uint8_t *sZero = reinterpret_cast<uint8_t *>(sStage) + 2 * C::kStageBytes;
-  int32_t *sCol = reinterpret_cast<int32_t *>(sZero + C::kZeroBytes);
-  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sCol) + 2048);
+  int32_t *sCol = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(sStage) + 2 * C::kStageBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sCol) + C::kColBytes);
   uint64_t *empty = full + C::kStages;
   uint64_t *tfull = empty + C::kStages;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
+  int32_t *sIdx = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(full) + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int u_begin = __ldg(args.sched_off + blockIdx.x);
   const int u_end = __ldg(args.sched_off + blockIdx.x + 1);
+  const int s_begin = __ldg(args.stream_off + blockIdx.x);
+  const int n_st = __ldg(args.stream_off + blockIdx.x + 1) - s_begin;
+
   if (threadIdx.x == 0) trace_evt(args, 7, 0);  // CTA start
 
   if (threadIdx.x == 0) {
@@ -219,9 +219,6 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     }
     ptx::fence_mbar_init();
   }
-  for (int i = threadIdx.x; i < (int)(C::kZeroBytes / 16); i += kThreads)
-    reinterpret_cast<uint4 *>(sZero)[i] = make_uint4(0, 0, 0, 0);
-  ptx::fence_proxy_async_smem();  // the zero buffer is read by the TMA (async proxy)
   if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
@@ -245,92 +242,143 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int64_t pitch = args.lda * 2;
     int stage = 0;
     uint32_t phase = 0;
-    int sc = 0;
-    int4 su_next = u_begin < u_end ? __ldg(args.sched + u_begin) : make_int4(0, 0, 0, 0);
-    for (int j = u_begin; j < u_end; ++j) {
-      const int4 su = su_next;
-      if (j + 1 < u_end) su_next = __ldg(args.sched + j + 1);
-      const TileMeta t = args.tiles[su.x];
-      if (threadIdx.x == 0) trace_evt(args, j - u_begin, 0);
-      const int m0 = su.y;
-      const bool active = chunk < su.z * 16;  // token half present in this unit
-      const int mcol = m0 + chunk * 8;
+    int32_t *ring = sIdx + warp * (kIdxSlots * kSlotInts);  // this warp's index ring
+    // stage k's 16 row indices of this warp (lanes 0-3) + record (lane 4)
+    auto prefetch = [&](int k) {
+      if (lane < 5) {
+        const int32_t *src = args.stream + (int64_t)(s_begin + k) * kIdxInts + (lane < 4 ? warp * 16 + lane * 4 : 64);
+        ptx::cp_async_16(ring + (k % kIdxSlots) * kSlotInts + lane * 4, src, 16);
+      }
+    };
+    for (int k = 0; k < kIdxLook; ++k) {  // one cp.async group per prefetched stage
+      if (k < n_st) prefetch(k);
+      ptx::cp_async_commit();
+    }
+    for (int i = 0; i < n_st; ++i) {
+      const int32_t *slot = ring + (i % kIdxSlots) * kSlotInts;
+      const long long c0 = clock64();
+      ptx::mbar_wait(&empty[stage], phase ^ 1);
+      const long long c1 = clock64();
+      // stage i's indices were the (kIdxLook)-th most recent group
+      ptx::cp_async_wait_group<kIdxLook - 1>();
+      __syncwarp();
+      const long long c2 = clock64();
+      const int4 rec = *reinterpret_cast<const int4 *>(slot + 16);
+      if (threadIdx.x == 0 && (rec.w & (1 << 16))) trace_evt(args, rec.w & 0xffff, 0);
+      const int nh = rec.z & 0xf;
+      const bool active = chunk < nh * 16;  // token half present in this unit
+      const int mcol = rec.y + chunk * 8;
       const uint32_t src_bytes_m =
           !active ? 0u : (mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u));
       const char *lane_base = at_bytes + (src_bytes_m ? (int64_t)mcol * 2 : 0);
-      const int32_t *ki = args.kidx + t.kidx_off + warp * 16 + (lane & 15);
-      const uint8_t *wsrc = args.wimg + t.w_off;
-      int64_t off_next = (int64_t)__ldg(ki) * pitch;
-      for (int kb = 0; kb < t.nkb; ++kb) {
-        const int64_t off_mine = off_next;
-        if (kb + 1 < t.nkb) off_next = (int64_t)__ldg(ki + (kb + 1) * kBlockK) * pitch;
-        const int rows_valid = t.k_i - kb * kBlockK - warp * 16;  // rows of this warp holding real kept k
-        ptx::mbar_wait(&empty[stage], phase ^ 1);
-        if (warp == 0 && lane == 0) {
+      if (warp == 0 && lane == 0) {
+        if (args.debug & 64) {  // experiment: no weight copy
+          ptx::mbar_arrive(&full[stage]);
+        } else {
           ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes);
-          ptx::bulk_g2s(sB + stage * C::kBBytes, wsrc + (int64_t)kb * args.wbytes, (uint32_t)args.wbytes,
-                        &full[stage], keep);
+          ptx::bulk_g2s(sB + stage * C::kBBytes, args.wimg + rec.x, (uint32_t)args.wbytes, &full[stage], keep);
         }
-        uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + warp * 16 * 128;
+      }
+      uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + warp * 16 * 128;
+      // all 16 row indices into registers BEFORE the first cp.async: a shared
+      // load issued after a cp.async waits for it in the same (MIO) pipe
+      int rows[16];
+#pragma unroll
+      for (int v4 = 0; v4 < 4; ++v4) {
+        const int4 r4 = reinterpret_cast<const int4 *>(slot)[v4];
+        rows[4 * v4] = r4.x; rows[4 * v4 + 1] = r4.y; rows[4 * v4 + 2] = r4.z; rows[4 * v4 + 3] = r4.w;
+      }
+      // Fast path (warp-uniform): every row real and the unit's full token
+      // range inside M -> plain 16-byte cp.async.  The zero-fill form (with a
+      // source-size operand) only for padded rows / ragged token blocks.
+      int min_row = rows[0];
+#pragma unroll
+      for (int r = 1; r < 16; ++r) min_row = min(min_row, rows[r]);
+      const bool fast = min_row >= 0 && nh == C::kHalves && rec.y + TB <= args.M && !(args.debug & 256);
+      if (fast) {
+#pragma unroll
+        for (int it = 0; it < 16 / kRowsPerInst; ++it) {
+          const int rl = it * kRowsPerInst + rsub;
+          const int row = kRowsPerInst == 1 ? rows[it] : (rsub ? rows[it * kRowsPerInst + 1] : rows[it * kRowsPerInst]);
+          ptx::cp_async_16_full(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), lane_base + (int64_t)row * pitch);
+        }
+      } else {
 #pragma unroll
         for (int it = 0; it < 16 / kRowsPerInst; ++it) {
           const int rl = it * kRowsPerInst + rsub;  // row within this warp's 16
-          const int64_t roff = __shfl_sync(0xffffffffu, off_mine, rl);
-          const uint32_t nbytes = rl < rows_valid ? src_bytes_m : 0u;
-          if (active) ptx::cp_async_16(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), nbytes ? lane_base + roff : at_bytes, nbytes);
+          const int row = kRowsPerInst == 1 ? rows[it] : (rsub ? rows[it * kRowsPerInst + 1] : rows[it * kRowsPerInst]);
+          const uint32_t nbytes = row >= 0 ? src_bytes_m : 0u;
+          if (active)
+            ptx::cp_async_16(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16),
+                             nbytes ? lane_base + (int64_t)row * pitch : at_bytes, nbytes);
         }
-        ptx::cp_async_mbar_arrive_noinc(&full[stage]);
-        if (threadIdx.x == 0) trace_stage(args, sc, 0);
-        ++sc;
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
-      if (threadIdx.x == 0) trace_evt(args, j - u_begin, 1);
+      // Slot (i + kIdxLook) % kIdxSlots last held stage i + kIdxLook - kIdxSlots,
+      // which this warp has issued and the MMA warp has committed (we passed
+      // empty[i], so stage i - kStages is consumed): free to overwrite.
+      if (i + kIdxLook < n_st) prefetch(i + kIdxLook);
+      ptx::cp_async_mbar_arrive_noinc(&full[stage]);  // also covers the prefetch
+      ptx::cp_async_commit();
+      if (threadIdx.x == 0) trace_stage(args, i, 0);
+      if (threadIdx.x == 0 && args.trace != nullptr && i < 32) {
+        const long long c3 = clock64();
+        args.trace[(int64_t)gridDim.x * 64 + ((int64_t)blockIdx.x * 32 + i) * 4 + 3] =
+            (min(c1 - c0, 0xfffffLL) << 40) | (min(c2 - c1, 0xfffffLL) << 20) | min(c3 - c2, 0xfffffLL);
+      }
+      if (threadIdx.x == 0 && (rec.w & (1 << 17))) trace_evt(args, rec.w & 0xffff, 1);
+      if (++stage == C::kStages) { stage = 0; phase ^= 1; }
     }
+    ptx::cp_async_wait_group<0>();
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------ MMA issuer
+    // Walks the same stage stream (records from the shared index ring).
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t a_base = ptx::smem_u32(sA);
     const uint32_t b_base = ptx::smem_u32(sB);
-    int sc = 0;
-    for (int j = u_begin; j < u_end; ++j) {
-      const int4 su = __ldg(args.sched + j);
-      const TileMeta t = args.tiles[su.x];
-      const uint32_t n_mma = (uint32_t)((t.n_i + 15) & ~15);
+    uint32_t d_tmem = tmem_base;
+    for (int i = 0; i < n_st; ++i) {
+      // full[stage] includes producer warp 0's cp.async arrival for stage i,
+      // which covers its prefetch of stage i's record into its ring
+      ptx::mbar_wait(&full[stage], phase);
+      if (lane == 0) trace_stage(args, i, 1);
+      const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kIdxSlots) * kSlotInts + 16);
+      const int nh = rec.z & 0xf, nk = (rec.z >> 4) & 0xf;
+      const uint32_t n_mma = (uint32_t)(rec.z >> 8);
       const uint32_t idesc = args.idesc | ((n_mma >> 3) << 17);
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * C::kAccCols);
-      ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-      ptx::tc_fence_after();
-      if (lane == 0) trace_evt(args, j - u_begin, 2);
-      for (int kb = 0; kb < t.nkb; ++kb) {
-        ptx::mbar_wait(&full[stage], phase);
-        if (lane == 0) trace_stage(args, sc, 1);
-        if (!(args.debug & 8)) ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
+      const bool first = rec.w & (1 << 16), last = rec.w & (1 << 17);
+      if (first) {
+        d_tmem = tmem_base + (uint32_t)(acc * C::kAccCols);
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const int nk = min(4, t.k16 - kb * 4);
-        if (ptx::elect_one()) {
-          for (int kk = 0; kk < nk; ++kk) {
-            const uint64_t bdesc = ptx::make_sw128_desc(b_base + stage * C::kBBytes + kk * 32, 16, 1024);
-            for (int h = 0; h < su.z; ++h) {
-              const uint64_t adesc =
-                  ptx::make_sw128_desc(a_base + stage * C::kABytes + h * 16384 + kk * 2048, 8192, 1024);
-              if (!(args.debug & 4)) ptx::mma_f16_ss(d_tmem + h * 128, adesc, bdesc, idesc, (kb | kk) != 0 ? 1u : 0u);
-            }
-          }
-          ptx::mma_commit(&empty[stage]);
-        }
-        __syncwarp();
-        if (lane == 0) trace_stage(args, sc, 2);
-        ++sc;
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        if (lane == 0) trace_evt(args, rec.w & 0xffff, 2);
       }
-      if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
+      if (!(args.debug & 8)) ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
+      ptx::tc_fence_after();
+      if (ptx::elect_one()) {
+        for (int kk = 0; kk < nk; ++kk) {
+          const uint64_t bdesc = ptx::make_sw128_desc(b_base + stage * C::kBBytes + kk * 32, 16, 1024);
+          for (int h = 0; h < nh; ++h) {
+            const uint64_t adesc =
+                ptx::make_sw128_desc(a_base + stage * C::kABytes + h * 16384 + kk * 2048, 8192, 1024);
+            if (!(args.debug & 4))
+              ptx::mma_f16_ss(d_tmem + h * 128, adesc, bdesc, idesc, (first && kk == 0) ? 0u : 1u);
+          }
+        }
+        ptx::mma_commit(&empty[stage]);
+      }
       __syncwarp();
-      if (lane == 0) trace_evt(args, j - u_begin, 3);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (lane == 0) trace_stage(args, i, 2);
+      if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      if (last) {
+        if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
+        __syncwarp();
+        if (lane == 0) trace_evt(args, rec.w & 0xffff, 3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
     }
   } else {
     // ------------------------------------------------ epilogue (8 warps)
@@ -339,9 +387,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     const int h = e >> 2;             // TMEM column half (token half for TB=256, column half for TB=128)
     const bool vec = ((args.ldc * (int64_t)sizeof(OutT)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
-    const bool bulk_ok = vec && ((int64_t)args.M * (int64_t)sizeof(OutT)) % 16 == 0;
-    // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... whenever it
-    // would otherwise wait for an accumulator, and the rest at the end
+    // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... while it
+    // waits for an accumulator (policy 0: any unit; 1: the CTA's last unit
+    // only, i.e. once the producer has finished gathering -- a store stream
+    // on the same SM throttles the gathers; 2: none), and the rest at the end
     int zr = __ldg(args.zero_off + blockIdx.x) + e;
     const int z1 = (args.accumulate || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
     constexpr int V = 16 / (int)sizeof(OutT);  // tokens per 16-byte store
@@ -354,14 +403,15 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       const int m0 = su.y, nh = su.z;
       // col ids double-buffered by unit parity: a fast warp may fill the next
       // unit's table while others still store this unit's last chunk
-      int32_t *ucol = sCol + ((j - u_begin) & 1) * 256;
+      int32_t *ucol = sCol + ((j - u_begin) & 1) * BN;
       if (et < BN) ucol[et] = et < t.n_i ? __ldg(args.colids + t.col_off + et) : -1;
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 4);
       // wait for the accumulator, writing zero rows meanwhile
       // (non-blocking test_wait while there is filler work: try_wait would
       // suspend the warp for up to its time limit between zero rows)
-      while (zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
-        zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok && (args.debug & 32), vec, sZero, C::kZeroBytes);
+      const bool fill = args.zero_policy == 0 || (args.zero_policy == 1 && j == u_end - 1);
+      while (fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
+        write_zero_row<OutT>(args, __ldg(args.zero_rows + zr), lane, vec);
         zr += kEpiWarps;
       }
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -370,22 +420,23 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 5);
       const uint32_t t_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::kAccCols) + h * 128;
       const int n_half0 = min(t.n_i, 128);
-      const int n_chunks = (n_half0 + 31) / 32;
+      constexpr int CK = C::kChunk;
+      const int n_chunks = (n_half0 + CK - 1) / CK;
       const int seg = TB == 256 ? nh * 128 : 128;  // tokens per output row segment
       for (int ci = 0; ci < n_chunks; ++ci) {
-        const int c0 = ci * 32;
+        const int c0 = ci * CK;
         float *buf = sStage + (ci & 1) * (C::kStageBytes / 4);  // double-buffered staging
         // 1) TMEM -> registers -> staging buffer [col][token] (conflict-free)
-        const bool have = TB == 256 ? (h < nh) : (h * 128 + c0 < t.n_i);
+        const bool have = (TB == 256 ? (h < nh) : (h * 128 + c0 < t.n_i)) && !(args.debug & 128);
         if (have) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)c0, v);
+          uint32_t v[CK];
+          ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, v);
           ptx::tmem_ld_wait();
           if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 0);
           const int tok = (TB == 256 ? h * 128 : 0) + q * 32 + lane;
-          float *dst = buf + (TB == 256 ? 0 : h * 32 * TB) + tok;
+          float *dst = buf + (TB == 256 ? 0 : h * CK * TB) + tok;
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) dst[jj * TB] = __uint_as_float(v[jj]);
+          for (int jj = 0; jj < CK; ++jj) dst[jj * TB] = __uint_as_float(v[jj]);
         }
         if (ci == n_chunks - 1) {
           // all of this warp's TMEM reads for the unit are done: hand the
@@ -399,28 +450,44 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         // whose buffer chunk ci + 1 will overwrite.
         epi_sync();
         if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 2);
-        // 2) staged rows -> global, one C^T row segment at a time
-        constexpr int kRows = C::kStageCols;              // 32 (TB=256) | 64 (TB=128)
-        constexpr int kRowsPerWarp = kRows / kEpiWarps;   // 4 | 8
+        // 2) staged rows -> global, one C^T row segment at a time.  All of
+        // this warp's shared-memory reads are issued before its first global
+        // store: an LDS queued behind a backpressured STG in the same pipe
+        // would wait for it, serializing the loop at DRAM-queue latency.
+        constexpr int kRows = C::kStageCols;              // 16 (TB=256) | 32 (TB=128)
+        constexpr int kRowsPerWarp = kRows / kEpiWarps;   // 2 | 4
+        constexpr int NIT = (TB / V + 31) / 32;           // 16-byte pieces per lane per row
+        float vals[kRowsPerWarp][NIT][V];
+        int orows[kRowsPerWarp];
 #pragma unroll
         for (int rr = 0; rr < kRowsPerWarp; ++rr) {
           const int srow = e * kRowsPerWarp + rr;
-          const int col = TB == 256 ? c0 + srow : (srow < 32 ? c0 + srow : 128 + c0 + (srow - 32));
-          const int orow = col < t.n_i ? ucol[col] : -1;
-          if (orow < 0 || (args.debug & 2)) continue;
-          OutT *grow = out + (int64_t)orow * args.ldc + m0;
+          const int col = TB == 256 ? c0 + srow : (srow < CK ? c0 + srow : 128 + c0 + (srow - CK));
+          orows[rr] = (col < t.n_i && !(args.debug & 2)) ? ucol[col] : -1;
           const float *srow_p = buf + srow * TB;
-          for (int tk = lane * V; tk < seg; tk += 32 * V) {
-            float vals[V];
+#pragma unroll
+          for (int n = 0; n < NIT; ++n) {
+            const int tk = (n * 32 + lane) * V;
 #pragma unroll
             for (int x = 0; x < V; x += 4) {
-              const float4 f = *reinterpret_cast<const float4 *>(srow_p + tk + x);
-              vals[x] = f.x; vals[x + 1] = f.y; vals[x + 2] = f.z; vals[x + 3] = f.w;
+              const float4 f = tk < seg ? *reinterpret_cast<const float4 *>(srow_p + tk + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+              vals[rr][n][x] = f.x; vals[rr][n][x + 1] = f.y; vals[rr][n][x + 2] = f.z; vals[rr][n][x + 3] = f.w;
             }
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+          if (orows[rr] < 0) continue;
+          OutT *grow = out + (int64_t)orows[rr] * args.ldc + m0;
+#pragma unroll
+          for (int n = 0; n < NIT; ++n) {
+            const int tk = (n * 32 + lane) * V;
+            if (tk >= seg) continue;
+            float *v = vals[rr][n];
             if (vec && m0 + tk + V <= args.M) {
               uint4 *p = reinterpret_cast<uint4 *>(grow + tk);
-              if (args.accumulate) unpack16_add<OutT>(*p, vals);
-              const uint4 pk = pack16<OutT>(vals);
+              if (args.accumulate) unpack16_add<OutT>(*p, v);
+              const uint4 pk = pack16<OutT>(v);
               if (args.debug & 16) {  // experiment: staging reads without the global store
                 if ((pk.x ^ pk.y ^ pk.z ^ pk.w) == 0x7fc00001u) __stcs(p, pk);
               } else {
@@ -430,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 #pragma unroll
               for (int x = 0; x < V; ++x) {
                 if (m0 + tk + x < args.M) {
-                  float r = vals[x];
+                  float r = v[x];
                   if (args.accumulate) r += cvt_in<OutT>(grow[tk + x]);
                   grow[tk + x] = cvt_out<OutT>(r);
                 }
@@ -444,11 +511,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    for (; zr < z1; zr += kEpiWarps)
-      zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok && (args.debug & 32), vec, sZero, C::kZeroBytes);
+    for (; zr < z1; zr += kEpiWarps) write_zero_row<OutT>(args, __ldg(args.zero_rows + zr), lane, vec);
     if (e == 0 && lane == 0) trace_evt(args, 7, 1);  // last zero row issued
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // bulk stores done before exit
-    if (e == 0 && lane == 0) trace_evt(args, 7, 2);  // bulk stores drained
   }
 
   __syncthreads();

@@ -61,6 +61,15 @@ struct HostSchedule {
   std::vector<int32_t> units;  // 4 ints per unit
   std::vector<int32_t> off;    // grid + 1
   std::vector<int32_t> zoff;   // grid + 1
+  // Per-CTA stage streams: stage s of CTA c (s in [soff[c], soff[c+1])) is
+  // one 64-k block of one unit: stream[68 s .. 68 s + 64) are its kept A^T
+  // row indices (-1 = padding -> zero fill), stream[68 s + 64 .. + 68) the
+  // record {weight-image byte offset, first token, halves | k-steps << 4 |
+  // MMA N << 8, unit-in-CTA | first-block << 16 | last-block << 17}.  The
+  // kernel streams it into shared memory with TMA, so the producer's index
+  // loads never wait behind its own gathers.
+  std::vector<int32_t> stream;
+  std::vector<int32_t> soff;   // grid + 1
   double makespan_ns = 0, mean_ns = 0;
 };
 int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows, int sms, int tb,
@@ -76,6 +85,8 @@ struct GemmArgs {
   const int4 *sched;         // per-CTA unit lists (HostSchedule::units)
   const int32_t *sched_off;  // grid + 1
   const int32_t *zero_off;   // grid + 1
+  const int32_t *stream;     // HostSchedule::stream
+  const int32_t *stream_off; // grid + 1
   void *out;
   int64_t ldc;
   const void *at;     // A^T (K x M, 16-bit), row stride lda
@@ -86,6 +97,7 @@ struct GemmArgs {
   uint32_t idesc;     // instruction descriptor without the N field
   int32_t block_n;
   int64_t *trace;     // optional per-CTA event timeline (tw_gemm_traced), else null
+  int32_t zero_policy; // when the epilogue writes zero rows (kernel comment); env TW_B200_ZERO
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };
 
@@ -105,6 +117,8 @@ struct tw_dev_schedule {
   int4 *units = nullptr;
   int32_t *off = nullptr;
   int32_t *zoff = nullptr;
+  int32_t *stream = nullptr;
+  int32_t *soff = nullptr;
 };
 
 // Device side of a plan (defined in tw_capi.cu).

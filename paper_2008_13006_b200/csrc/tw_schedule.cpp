@@ -18,6 +18,7 @@
 #include <cmath>
 #include <functional>
 #include <numeric>
+#include <climits>
 #include <queue>
 
 #include "tw_internal.h"
@@ -183,6 +184,32 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
     s.zoff[(size_t)c + 1] = (int32_t)(s.zoff[(size_t)c] + (best_z.empty() ? 0 : best_z[(size_t)c]));
   }
   if (s.zoff[(size_t)G] != Z) return fail(TW_ERR_ARG, "internal: zero-row schedule does not cover the zero list");
+  // per-CTA stage streams (see HostSchedule)
+  const int64_t wbytes = (int64_t)hp.wrows * 128;
+  s.soff.assign((size_t)G + 1, 0);
+  int64_t n_stages = 0;
+  for (int c = 0; c < G; ++c) {
+    for (int32_t u = s.off[(size_t)c]; u < s.off[(size_t)c + 1]; ++u) {
+      const int32_t *un = &s.units[(size_t)u * 4];
+      const TileMeta &t = hp.tiles[(size_t)un[0]];
+      const int32_t n_mma = (t.n_i + 15) & ~15;
+      for (int kb = 0; kb < t.nkb; ++kb) {
+        for (int r = 0; r < 64; ++r) {
+          const int32_t idx = hp.kidx[(size_t)t.kidx_off + (size_t)kb * 64 + (size_t)r];
+          s.stream.push_back(kb * 64 + r < t.k_i && idx < hp.k ? idx : -1);
+        }
+        const int64_t woff = t.w_off + kb * wbytes;
+        if (woff > INT32_MAX) return fail(TW_ERR_UNSUPPORTED, "weight image larger than 2 GiB");
+        const int32_t nk = std::min(4, t.k16 - kb * 4);
+        s.stream.insert(s.stream.end(),
+                        {(int32_t)woff, un[1], un[2] | (nk << 4) | (n_mma << 8),
+                         (u - s.off[(size_t)c]) | (kb == 0 ? 1 << 16 : 0) | (kb == t.nkb - 1 ? 1 << 17 : 0)});
+        ++n_stages;
+      }
+    }
+    if (n_stages > INT32_MAX / 68) return fail(TW_ERR_UNSUPPORTED, "schedule too long");
+    s.soff[(size_t)c + 1] = (int32_t)n_stages;
+  }
   s.makespan_ns = best_total;
   s.mean_ns = (total + Z * zc) / G;
   return TW_OK;

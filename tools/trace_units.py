@@ -49,8 +49,11 @@ def main():
         at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
     dt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[args.out_dtype]
     out = torch.empty((n, m), dtype=dt, device="cuda")
-    sms = ctypes.c_int(0)
-    _lib.call("tw_device_sm_count", ctypes.byref(sms))
+    sms_dev = ctypes.c_int(0)
+    _lib.call("tw_device_sm_count", ctypes.byref(sms_dev))
+    # the trace is indexed by the launch grid (the schedule's CTA count)
+    _, unit_off, _ = plan.schedule(m, args.out_dtype, sms=int(os.environ.get("TW_B200_SMS", sms_dev.value)))
+    sms = ctypes.c_int(len(unit_off) - 1)
     trace = torch.zeros(sms.value * (64 + 128 + 32), dtype=torch.int64, device="cuda")
     code = {"fp32": 0, "bf16": 1, "fp16": 2}[args.out_dtype]
     stream = torch.cuda.current_stream().cuda_stream
@@ -89,6 +92,13 @@ def main():
         c0 = srel[0, si]
         print(f"{si:5d} {np.nanmedian(srel[:, si, 0]):9.2f} {np.nanmedian(srel[:, si, 1]):9.2f} "
               f"{np.nanmedian(srel[:, si, 2]):9.2f}     [{c0[0]:7.2f} {c0[1]:7.2f} {c0[2]:7.2f}]")
+    raw3 = full[sms.value * 64: sms.value * 192].reshape(sms.value, 32, 4)[:, :, 3].astype(np.int64)
+    print("producer cycles per stage (median over CTAs): wait_empty wait_idx issue")
+    for si in range(12):
+        v = raw3[:, si]
+        v = v[v > 0]
+        if v.size:
+            print(f"  stage {si:2d}: {np.median(v >> 40):7.0f} {np.median((v >> 20) & 0xfffff):7.0f} {np.median(v & 0xfffff):7.0f}")
     base = np.where(ep[:, :1] > 0, ep[:, :1], np.nan)
     erel = np.where(ep > 0, ep - base, np.nan)  # SM cycles since chunk 0's TMEM load completed
     print("epilogue chunk c of unit 0 (median over CTAs, SM cycles from chunk-0 ld): ld_done sts_done synced stored")
