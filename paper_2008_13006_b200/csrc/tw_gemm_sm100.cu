@@ -68,7 +68,7 @@ struct Cfg {
   static constexpr uint32_t kBBytes = BN * 128;               // 16 KB | 32 KB
   static constexpr uint32_t kAccCols = 256;                   // TMEM columns per accumulator
   static constexpr uint32_t kTmemCols = 2 * kAccCols;
-  static constexpr int kChunk = 16;                           // accumulator columns per epilogue chunk
+  static constexpr int kChunk = 32;                           // accumulator columns per epilogue chunk
   static constexpr int kStageCols = kHalves == 2 ? kChunk : 2 * kChunk;  // staged C^T rows per chunk
   static constexpr uint32_t kStageBytes = kStageCols * TB * 4;          // 16 KB; two are used
   static constexpr uint32_t kColBytes = 2 * BN * 4;                     // col-id table, double buffered
@@ -423,14 +423,18 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       constexpr int CK = C::kChunk;
       const int n_chunks = (n_half0 + CK - 1) / CK;
       const int seg = TB == 256 ? nh * 128 : 128;  // tokens per output row segment
+      // this warp reads TMEM for chunk c iff its column half / token half exists
+      auto have_chunk = [&](int c) {
+        return (TB == 256 ? (h < nh) : (h * 128 + c * CK < t.n_i)) && !(args.debug & 128);
+      };
+      uint32_t v[CK];  // TMEM chunk in flight: loaded one chunk ahead of its use
+      if (have_chunk(0)) ptx::tmem_ld_32x32b_x32(t_base, v);
       for (int ci = 0; ci < n_chunks; ++ci) {
         const int c0 = ci * CK;
         float *buf = sStage + (ci & 1) * (C::kStageBytes / 4);  // double-buffered staging
         // 1) TMEM -> registers -> staging buffer [col][token] (conflict-free)
-        const bool have = (TB == 256 ? (h < nh) : (h * 128 + c0 < t.n_i)) && !(args.debug & 128);
+        const bool have = have_chunk(ci);
         if (have) {
-          uint32_t v[CK];
-          ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, v);
           ptx::tmem_ld_wait();
           if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 0);
           const int tok = (TB == 256 ? h * 128 : 0) + q * 32 + lane;
@@ -449,57 +453,64 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         // buffering) guarantees every warp finished storing chunk ci - 1,
         // whose buffer chunk ci + 1 will overwrite.
         epi_sync();
+        // next chunk's TMEM load overlaps this chunk's global stores
+        if (ci + 1 < n_chunks && have_chunk(ci + 1)) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)(c0 + CK), v);
         if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 2);
         // 2) staged rows -> global, one C^T row segment at a time.  All of
         // this warp's shared-memory reads are issued before its first global
         // store: an LDS queued behind a backpressured STG in the same pipe
         // would wait for it, serializing the loop at DRAM-queue latency.
-        constexpr int kRows = C::kStageCols;              // 16 (TB=256) | 32 (TB=128)
-        constexpr int kRowsPerWarp = kRows / kEpiWarps;   // 2 | 4
+        constexpr int kRows = C::kStageCols;              // 32 (TB=256) | 64 (TB=128)
+        constexpr int kRowsPerWarp = kRows / kEpiWarps;   // 4 | 8
         constexpr int NIT = (TB / V + 31) / 32;           // 16-byte pieces per lane per row
-        float vals[kRowsPerWarp][NIT][V];
-        int orows[kRowsPerWarp];
+        constexpr int kBatch = kRowsPerWarp * NIT * V > 32 ? 32 / (NIT * V) : kRowsPerWarp;  // rows per load batch
 #pragma unroll
-        for (int rr = 0; rr < kRowsPerWarp; ++rr) {
-          const int srow = e * kRowsPerWarp + rr;
-          const int col = TB == 256 ? c0 + srow : (srow < CK ? c0 + srow : 128 + c0 + (srow - CK));
-          orows[rr] = (col < t.n_i && !(args.debug & 2)) ? ucol[col] : -1;
-          const float *srow_p = buf + srow * TB;
+        for (int r0 = 0; r0 < kRowsPerWarp; r0 += kBatch) {
+          float vals[kBatch][NIT][V];
+          int orows[kBatch];
 #pragma unroll
-          for (int n = 0; n < NIT; ++n) {
-            const int tk = (n * 32 + lane) * V;
+          for (int rb = 0; rb < kBatch; ++rb) {
+            const int srow = e * kRowsPerWarp + r0 + rb;
+            const int col = TB == 256 ? c0 + srow : (srow < CK ? c0 + srow : 128 + c0 + (srow - CK));
+            orows[rb] = (col < t.n_i && !(args.debug & 2)) ? ucol[col] : -1;
+            const float *srow_p = buf + srow * TB;
 #pragma unroll
-            for (int x = 0; x < V; x += 4) {
-              const float4 f = tk < seg ? *reinterpret_cast<const float4 *>(srow_p + tk + x) : make_float4(0.f, 0.f, 0.f, 0.f);
-              vals[rr][n][x] = f.x; vals[rr][n][x + 1] = f.y; vals[rr][n][x + 2] = f.z; vals[rr][n][x + 3] = f.w;
+            for (int n = 0; n < NIT; ++n) {
+              const int tk = (n * 32 + lane) * V;
+#pragma unroll
+              for (int x = 0; x < V; x += 4) {
+                const float4 f =
+                    tk < seg ? *reinterpret_cast<const float4 *>(srow_p + tk + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+                vals[rb][n][x] = f.x; vals[rb][n][x + 1] = f.y; vals[rb][n][x + 2] = f.z; vals[rb][n][x + 3] = f.w;
+              }
             }
           }
-        }
 #pragma unroll
-        for (int rr = 0; rr < kRowsPerWarp; ++rr) {
-          if (orows[rr] < 0) continue;
-          OutT *grow = out + (int64_t)orows[rr] * args.ldc + m0;
+          for (int rb = 0; rb < kBatch; ++rb) {
+            if (orows[rb] < 0) continue;
+            OutT *grow = out + (int64_t)orows[rb] * args.ldc + m0;
 #pragma unroll
-          for (int n = 0; n < NIT; ++n) {
-            const int tk = (n * 32 + lane) * V;
-            if (tk >= seg) continue;
-            float *v = vals[rr][n];
-            if (vec && m0 + tk + V <= args.M) {
-              uint4 *p = reinterpret_cast<uint4 *>(grow + tk);
-              if (args.accumulate) unpack16_add<OutT>(*p, v);
-              const uint4 pk = pack16<OutT>(v);
-              if (args.debug & 16) {  // experiment: staging reads without the global store
-                if ((pk.x ^ pk.y ^ pk.z ^ pk.w) == 0x7fc00001u) __stcs(p, pk);
+            for (int n = 0; n < NIT; ++n) {
+              const int tk = (n * 32 + lane) * V;
+              if (tk >= seg) continue;
+              float *v = vals[rb][n];
+              if (vec && m0 + tk + V <= args.M) {
+                uint4 *p = reinterpret_cast<uint4 *>(grow + tk);
+                if (args.accumulate) unpack16_add<OutT>(*p, v);
+                const uint4 pk = pack16<OutT>(v);
+                if (args.debug & 16) {  // experiment: staging reads without the global store
+                  if ((pk.x ^ pk.y ^ pk.z ^ pk.w) == 0x7fc00001u) __stcs(p, pk);
+                } else {
+                  __stcs(p, pk);
+                }
               } else {
-                __stcs(p, pk);
-              }
-            } else {
 #pragma unroll
-              for (int x = 0; x < V; ++x) {
-                if (m0 + tk + x < args.M) {
-                  float r = v[x];
-                  if (args.accumulate) r += cvt_in<OutT>(grow[tk + x]);
-                  grow[tk + x] = cvt_out<OutT>(r);
+                for (int x = 0; x < V; ++x) {
+                  if (m0 + tk + x < args.M) {
+                    float r = v[x];
+                    if (args.accumulate) r += cvt_in<OutT>(grow[tk + x]);
+                    grow[tk + x] = cvt_out<OutT>(r);
+                  }
                 }
               }
             }
