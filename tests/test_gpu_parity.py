@@ -279,3 +279,17 @@ def test_concurrent_streams_same_plan():
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o, ref)
+
+
+@pytest.mark.gpu
+def test_sharded_plan_single_rank_equals_full_plan():
+    """ShardedTwPlan without a process group (world 1) is the whole layer."""
+    _need_gpu()
+    a, w, p = orc.bench_inputs(256, 384, 700, 128, 0.75, seed=21)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    at = device_at(a)
+    sp = tw.ShardedTwPlan(ts)
+    assert sp.world == 1 and sp.col_range == (0, 700)
+    got = sp.gemm(at).cpu().numpy()
+    full = tw.TwPlan(ts).gemm(at).cpu().numpy()
+    assert np.array_equal(got, full)
