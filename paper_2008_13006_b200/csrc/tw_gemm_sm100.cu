@@ -72,8 +72,9 @@ struct Cfg {
   static constexpr int kStageCols = kHalves == 2 ? kChunk : 2 * kChunk;  // staged C^T rows per chunk
   static constexpr uint32_t kStageBytes = kStageCols * TB * 4;          // 16 KB; two are used
   static constexpr uint32_t kColBytes = 2 * BN * 4;                     // col-id table, double buffered
-  static constexpr uint32_t kFixed =
-      1024 /*align slack*/ + 2 * kStageBytes + kColBytes + 256 /*barriers*/ + kProducerWarps * kIdxSlots * kSlotInts * 4;
+  static constexpr uint32_t kZeroBytes = 8192;  // zero source block for TMA zero-row stores
+  static constexpr uint32_t kFixed = 1024 /*align slack*/ + 2 * kStageBytes + kColBytes + 256 /*barriers*/ +
+                                     kProducerWarps * kIdxSlots * kSlotInts * 4 + kZeroBytes;
   // as many 64-k pipeline stages as fit next to the epilogue buffers (4 for
   // G <= 128): bytes in flight per SM set the gather throughput
   static constexpr int kStages = (int)((232448u - kFixed) / (kABytes + kBBytes)) > 4
@@ -150,6 +151,30 @@ __device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int l
   for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(0.f);
 }
 
+// One zero row by 1-D TMA bulk stores (up to 8 KB each) from the zeroed smem
+// block, issued by lane 0: zero rows never occupy the LSU that the gathers
+// need (tools/membench7.cu: 8 KB bulk stores reach 5.4 TB/s chip-wide).
+// Falls back to STG when the row is not 16-byte aligned / sized.
+template <typename OutT>
+__device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int lane, bool bulk_ok, bool vec,
+                                              const uint8_t *zero_buf, uint32_t zero_bytes) {
+  if (!bulk_ok) {
+    write_zero_row<OutT>(a, row, lane, vec);
+    return;
+  }
+  if (lane == 0) {
+    char *dst = reinterpret_cast<char *>(a.out) + (int64_t)row * a.ldc * (int64_t)sizeof(OutT);
+    const int64_t bytes = (int64_t)a.M * (int64_t)sizeof(OutT);
+    for (int64_t off = 0; off < bytes; off += zero_bytes) {
+      const uint32_t n = (uint32_t)min((int64_t)zero_bytes, bytes - off);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + off),
+                   "r"(ptx::smem_u32(zero_buf)), "r"(n)
+                   : "memory");
+    }
+    ptx::bulk_commit();
+  }
+}
+
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
 // committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
@@ -198,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
   int32_t *sIdx = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(full) + 256);
+  uint8_t *sZero = reinterpret_cast<uint8_t *>(sIdx + kProducerWarps * kIdxSlots * kSlotInts);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -219,6 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     }
     ptx::fence_mbar_init();
   }
+  for (int i = threadIdx.x; i < (int)(C::kZeroBytes / 16); i += kThreads)
+    reinterpret_cast<uint4 *>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  ptx::fence_proxy_async_smem();  // zero block is read by TMA (async proxy)
   if (warp == kMmaWarp) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
@@ -294,13 +323,13 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       int min_row = rows[0];
 #pragma unroll
       for (int r = 1; r < 16; ++r) min_row = min(min_row, rows[r]);
-      const bool fast = min_row >= 0 && nh == C::kHalves && rec.y + TB <= args.M && !(args.debug & 256);
+      const bool fast = min_row >= 0 && rec.y + nh * 128 <= args.M && !(args.debug & 256);
       if (fast) {
 #pragma unroll
         for (int it = 0; it < 16 / kRowsPerInst; ++it) {
           const int rl = it * kRowsPerInst + rsub;
           const int row = kRowsPerInst == 1 ? rows[it] : (rsub ? rows[it * kRowsPerInst + 1] : rows[it * kRowsPerInst]);
-          ptx::cp_async_16_full(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), lane_base + (int64_t)row * pitch);
+          if (active) ptx::cp_async_16_full(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), lane_base + (int64_t)row * pitch);
         }
       } else {
 #pragma unroll
@@ -387,6 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     const int h = e >> 2;             // TMEM column half (token half for TB=256, column half for TB=128)
     const bool vec = ((args.ldc * (int64_t)sizeof(OutT)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
+    const bool bulk_ok = vec && ((int64_t)args.M * (int64_t)sizeof(OutT)) % 16 == 0 && !(args.debug & 32);
     // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... while it
     // waits for an accumulator (policy 0: any unit; 1: the CTA's last unit
     // only, i.e. once the producer has finished gathering -- a store stream
@@ -394,6 +424,18 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     int zr = __ldg(args.zero_off + blockIdx.x) + e;
     const int z1 = (args.accumulate || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
     constexpr int V = 16 / (int)sizeof(OutT);  // tokens per 16-byte store
+    // TMA mode: one issuing thread stores zero rows 4 at a time by scatter4
+    // from the zeroed smem block (no LSU traffic)
+    const bool issuer = (e == 0 && lane == 0);
+    int zq = __ldg(args.zero_off + blockIdx.x);
+    auto tma_zero_group = [&]() {
+      int32_t rows[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rows[i] = zq + i < z1 ? __ldg(args.zero_rows + zq + i) : args.n_rows;
+      for (int c0 = 0; c0 < args.M; c0 += 128) ptx::tma_scatter4(&args.out_map, c0, rows, sZero);
+      ptx::bulk_commit();
+      zq += 4;
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
     OutT *out = reinterpret_cast<OutT *>(args.out);
@@ -410,9 +452,14 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       // (non-blocking test_wait while there is filler work: try_wait would
       // suspend the warp for up to its time limit between zero rows)
       const bool fill = args.zero_policy == 0 || (args.zero_policy == 1 && j == u_end - 1);
-      while (fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
-        write_zero_row<OutT>(args, __ldg(args.zero_rows + zr), lane, vec);
-        zr += kEpiWarps;
+      if (args.epi_tma) {
+        if (issuer)
+          while (fill && zq < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) tma_zero_group();
+      } else {
+        while (fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
+          zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
+          zr += kEpiWarps;
+        }
       }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
@@ -429,6 +476,52 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       };
       uint32_t v[CK];  // TMEM chunk in flight: loaded one chunk ahead of its use
       if (have_chunk(0)) ptx::tmem_ld_32x32b_x32(t_base, v);
+      if (args.epi_tma) {
+        // ---- TMA store epilogue: TMEM -> registers -> OutT staging laid out
+        // [group][row][128 tokens] (group = token half, or column half for
+        // G = 256) -> one thread scatters each 4 staged rows to their C^T rows
+        // with cp.async.bulk.tensor tile::scatter4 (rows >= n_i go to an
+        // out-of-range row and are dropped; tokens >= M are clipped).  No
+        // global store passes through the LSU, which the gathers need.
+        OutT *stg = reinterpret_cast<OutT *>(sStage);
+        constexpr int kBufElems = 2 * CK * 128;
+        auto issue_chunk = [&](int cc) {
+          const OutT *b = stg + (cc & 1) * kBufElems;
+          for (int g = 0; g < 2; ++g) {
+            if (TB == 256 ? g >= nh : g * 128 + cc * CK >= t.n_i) continue;
+            const int tok0 = m0 + (TB == 256 ? g * 128 : 0);
+            const int cbase = (TB == 256 ? 0 : g * 128) + cc * CK;
+            for (int r4 = 0; r4 < CK && cbase + r4 < t.n_i; r4 += 4) {
+              int32_t rows[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) rows[i] = cbase + r4 + i < t.n_i ? ucol[cbase + r4 + i] : args.n_rows;
+              if (!(args.debug & 2)) ptx::tma_scatter4(&args.out_map, tok0, rows, b + (g * CK + r4) * 128);
+            }
+          }
+          ptx::bulk_commit();
+        };
+        for (int ci = 0; ci < n_chunks; ++ci) {
+          const bool have = have_chunk(ci);
+          if (have) ptx::tmem_ld_wait();
+          if (ci == n_chunks - 1) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+          }
+          if (issuer) ptx::bulk_wait_read<0>();  // chunk ci - 2 (same buffer) has left smem
+          epi_sync();                            // buffer ci & 1 free; chunk ci - 1 staged
+          if (issuer && ci > 0) issue_chunk(ci - 1);
+          if (have) {
+            OutT *dst = stg + (ci & 1) * kBufElems + h * CK * 128 + q * 32 + lane;
+#pragma unroll
+            for (int jj = 0; jj < CK; ++jj) dst[jj * 128] = cvt_out<OutT>(__uint_as_float(v[jj]));
+            ptx::fence_proxy_async_smem();  // staged data is read by TMA (async proxy)
+          }
+          if (ci + 1 < n_chunks && have_chunk(ci + 1)) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)((ci + 1) * CK), v);
+          if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 3);
+        }
+        epi_sync();  // last chunk staged
+        if (issuer) issue_chunk(n_chunks - 1);
+      } else
       for (int ci = 0; ci < n_chunks; ++ci) {
         const int c0 = ci * CK;
         float *buf = sStage + (ci & 1) * (C::kStageBytes / 4);  // double-buffered staging
@@ -522,7 +615,16 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    for (; zr < z1; zr += kEpiWarps) write_zero_row<OutT>(args, __ldg(args.zero_rows + zr), lane, vec);
+    if (args.epi_tma) {
+      if (issuer) {
+        while (zq < z1) tma_zero_group();
+        ptx::bulk_wait<0>();  // all TMA stores performed before the CTA exits
+      }
+    } else {
+      for (; zr < z1; zr += kEpiWarps)
+        zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
+      if (lane == 0) ptx::bulk_wait<0>();  // bulk stores performed (and smem read) before exit
+    }
     if (e == 0 && lane == 0) trace_evt(args, 7, 1);  // last zero row issued
   }
 

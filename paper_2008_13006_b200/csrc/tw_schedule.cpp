@@ -117,7 +117,11 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
     }
   }
   const int64_t zero_ctas = Z > 0 ? (Z * m * ob + (256 << 10) - 1) / (256 << 10) : 0;
-  int G = (int)std::min<int64_t>(sms, std::max<int64_t>({(int64_t)base.size(), zero_ctas, (int64_t)1}));
+  // CTAs: enough for every unit -- or every 128-token half-unit, so small
+  // layers (fewer 256-token units than SMs) can spread over more SMs
+  int64_t halves = 0;
+  for (const Unit &u : base) halves += u.nh;
+  int G = (int)std::min<int64_t>(sms, std::max<int64_t>({halves, zero_ctas, (int64_t)1}));
   auto by_cost = [](const Unit &a, const Unit &b) {
     return a.cost != b.cost ? a.cost > b.cost : (a.tile != b.tile ? a.tile < b.tile : a.m0 < b.m0);
   };

@@ -284,7 +284,6 @@ def test_concurrent_streams_same_plan():
 @pytest.mark.gpu
 def test_sharded_plan_single_rank_equals_full_plan():
     """ShardedTwPlan without a process group (world 1) is the whole layer."""
-    _need_gpu()
     a, w, p = orc.bench_inputs(256, 384, 700, 128, 0.75, seed=21)
     ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
     at = device_at(a)
