@@ -27,41 +27,6 @@ int cuda_fail(cudaError_t e, const char *what) {
   return fail(TW_ERR_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-using EncodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiled encode_tiled() {
-  static EncodeTiled fn = [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (EncodeTiled) nullptr;
-    return reinterpret_cast<EncodeTiled>(p);
-  }();
-  return fn;
-}
-
-// Output map for the scatter4 epilogue: C^T as a 2-D tensor {M tokens, rows},
-// box {128 tokens, 1 row}.  False if the layout does not allow TMA stores.
-bool make_out_map(CUtensorMap *map, void *ct, int64_t m, int64_t rows, int64_t ldc, int out_dtype) {
-  EncodeTiled enc = encode_tiled();
-  const int eb = out_dtype == TW_F32 ? 4 : 2;
-  if (!enc || rows < 1 || (reinterpret_cast<uintptr_t>(ct) & 15) || (ldc * eb) % 16 || rows >= (int64_t)1 << 31)
-    return false;
-  const CUtensorMapDataType dt = out_dtype == TW_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
-                                 : out_dtype == TW_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
-                                                       : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)(ldc * eb)};
-  const cuuint32_t box[2] = {128, 1};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(map, dt, 2, ct, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-
 int sm_count_of_current(int *sms, int *major) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -281,18 +246,9 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 15) | ((128u >> 4) << 24);
   a.block_n = hp.block_n;
   a.trace = trace;
-  a.n_rows = (int32_t)n_rows;
-  // Epilogue store path.  Default: LSU (smem-staged 16-byte stores).
-  // TW_B200_EPI=tma selects TMA tile::scatter4 stores: correct (tested) but
-  // measured slower on B200 (~240 cycles per 4-row scatter4).
-  static const int epi_mode = [] {
-    const char *e = std::getenv("TW_B200_EPI");
-    return (e && std::strcmp(e, "tma") == 0) ? 1 : 0;
-  }();
-  a.epi_tma = (epi_mode == 1 && !accumulate && make_out_map(&a.out_map, ct, m, n_rows, ldc, out_dtype)) ? 1 : 0;
   static const int zero_policy = [] {
     const char *e = std::getenv("TW_B200_ZERO");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   a.zero_policy = zero_policy;
   if (trace) {  // experiment knobs only honoured on the profiling entry point

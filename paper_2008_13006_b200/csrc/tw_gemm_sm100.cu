@@ -175,6 +175,68 @@ __device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int la
   }
 }
 
+// Epilogue store phase: this warp's kRows staged rows (starting at staged
+// row r0; staged row r holds tile column col_of(r)) -> their C^T rows, SEG
+// tokens from token m0 (row stride RS floats in the staging buffer).
+template <typename OutT, int kRows, int RS, typename ColOf>
+__device__ __forceinline__ void store_rows(const GemmArgs &args, OutT *out, const float *buf, int r0, int lane, int m0,
+                                           int seg, ColOf col_of, const int32_t *ucol, int n_i, bool vec) {
+  constexpr int V = 16 / (int)sizeof(OutT);
+  constexpr int NIT = (RS / V + 31) / 32;  // 16-byte pieces per lane per row
+  constexpr int kBatch = kRows * NIT * V > 32 ? (32 / (NIT * V) > 0 ? 32 / (NIT * V) : 1) : kRows;
+#pragma unroll
+  for (int rb0 = 0; rb0 < kRows; rb0 += kBatch) {
+    float vals[kBatch][NIT][V];
+    int orows[kBatch];
+#pragma unroll
+    for (int rb = 0; rb < kBatch; ++rb) {
+      const int srow = r0 + rb0 + rb;
+      const int col = col_of(srow);
+      orows[rb] = (col < n_i && !(args.debug & 2)) ? ucol[col] : -1;
+      const float *srow_p = buf + srow * RS;
+#pragma unroll
+      for (int n = 0; n < NIT; ++n) {
+        const int tk = (n * 32 + lane) * V;
+#pragma unroll
+        for (int x = 0; x < V; x += 4) {
+          const float4 f = tk < seg ? *reinterpret_cast<const float4 *>(srow_p + tk + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+          vals[rb][n][x] = f.x; vals[rb][n][x + 1] = f.y; vals[rb][n][x + 2] = f.z; vals[rb][n][x + 3] = f.w;
+        }
+      }
+    }
+#pragma unroll
+    for (int rb = 0; rb < kBatch; ++rb) {
+      if (orows[rb] < 0) continue;
+      OutT *grow = out + (int64_t)orows[rb] * args.ldc + m0;
+#pragma unroll
+      for (int n = 0; n < NIT; ++n) {
+        const int tk = (n * 32 + lane) * V;
+        if (tk >= seg) continue;
+        float *v = vals[rb][n];
+        if (vec && m0 + tk + V <= args.M) {
+          uint4 *p = reinterpret_cast<uint4 *>(grow + tk);
+          if (args.accumulate) unpack16_add<OutT>(*p, v);
+          const uint4 pk = pack16<OutT>(v);
+          if (args.debug & 16) {  // experiment: staging reads without the global store
+            if ((pk.x ^ pk.y ^ pk.z ^ pk.w) == 0x7fc00001u) __stcs(p, pk);
+          } else {
+            __stcs(p, pk);
+          }
+        } else {
+#pragma unroll
+          for (int x = 0; x < V; ++x) {
+            if (m0 + tk + x < args.M) {
+              float r = v[x];
+              if (args.accumulate) r += cvt_in<OutT>(grow[tk + x]);
+              grow[tk + x] = cvt_out<OutT>(r);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
 // committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
@@ -411,31 +473,27 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     }
   } else {
     // ------------------------------------------------ epilogue (8 warps)
+    // Warp e reads TMEM lane quadrant q = warp % 4 (tokens 32q..32q+31 of a
+    // 128-token half); the warp pairs (e, e + 4) split the rest by `h`:
+    //   mode A (TB = 256, two token halves): h = token half, 32-column chunks;
+    //   mode B (TB = 128, G = 256):          h = 128-column half, 32-col chunks;
+    //   mode C (TB = 256, one token half):   h = which 32 columns of a 64-column
+    //                                         chunk -- all 8 warps stay busy.
+    // Per chunk: tcgen05.ld (issued one chunk ahead) -> staging [row][token]
+    // in smem -> each warp stores whole C^T row segments with 16-byte
+    // streaming stores (512 B of one row per instruction).
     const int e = warp - kEpiWarp0;   // 0..7
     const int et = e * 32 + lane;     // 0..255
-    const int q = warp & 3;           // TMEM lane quadrant this warp may access
-    const int h = e >> 2;             // TMEM column half (token half for TB=256, column half for TB=128)
+    const int q = warp & 3;
+    const int h = e >> 2;
     const bool vec = ((args.ldc * (int64_t)sizeof(OutT)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
     const bool bulk_ok = vec && ((int64_t)args.M * (int64_t)sizeof(OutT)) % 16 == 0 && !(args.debug & 32);
-    // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... while it
-    // waits for an accumulator (policy 0: any unit; 1: the CTA's last unit
-    // only, i.e. once the producer has finished gathering -- a store stream
-    // on the same SM throttles the gathers; 2: none), and the rest at the end
+    // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... (8 KB TMA
+    // bulk stores) while it waits for an accumulator (policy 0: any unit; 1:
+    // the CTA's last unit only; 2: none), and the rest at the end
     int zr = __ldg(args.zero_off + blockIdx.x) + e;
     const int z1 = (args.accumulate || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
-    constexpr int V = 16 / (int)sizeof(OutT);  // tokens per 16-byte store
-    // TMA mode: one issuing thread stores zero rows 4 at a time by scatter4
-    // from the zeroed smem block (no LSU traffic)
-    const bool issuer = (e == 0 && lane == 0);
-    int zq = __ldg(args.zero_off + blockIdx.x);
-    auto tma_zero_group = [&]() {
-      int32_t rows[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) rows[i] = zq + i < z1 ? __ldg(args.zero_rows + zq + i) : args.n_rows;
-      for (int c0 = 0; c0 < args.M; c0 += 128) ptx::tma_scatter4(&args.out_map, c0, rows, sZero);
-      ptx::bulk_commit();
-      zq += 4;
-    };
+    constexpr int CK = C::kChunk;              // 32 accumulator columns per TMEM load
     int acc = 0;
     uint32_t acc_phase = 0;
     OutT *out = reinterpret_cast<OutT *>(args.out);
@@ -452,88 +510,37 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       // (non-blocking test_wait while there is filler work: try_wait would
       // suspend the warp for up to its time limit between zero rows)
       const bool fill = args.zero_policy == 0 || (args.zero_policy == 1 && j == u_end - 1);
-      if (args.epi_tma) {
-        if (issuer)
-          while (fill && zq < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) tma_zero_group();
-      } else {
-        while (fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
-          zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
-          zr += kEpiWarps;
-        }
+      while (fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
+        zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
+        zr += kEpiWarps;
       }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       epi_sync();  // sCol visible; previous unit's staging reads done
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 5);
-      const uint32_t t_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::kAccCols) + h * 128;
-      const int n_half0 = min(t.n_i, 128);
-      constexpr int CK = C::kChunk;
-      const int n_chunks = (n_half0 + CK - 1) / CK;
-      const int seg = TB == 256 ? nh * 128 : 128;  // tokens per output row segment
-      // this warp reads TMEM for chunk c iff its column half / token half exists
-      auto have_chunk = [&](int c) {
-        return (TB == 256 ? (h < nh) : (h * 128 + c * CK < t.n_i)) && !(args.debug & 128);
-      };
+      const bool mode_a = TB == 256 && nh == 2;
+      const bool mode_c = TB == 256 && nh == 1;
+      const int ccols = mode_c ? 2 * CK : CK;  // tile columns per chunk
+      const int n_chunks = (min(t.n_i, 128) + ccols - 1) / ccols;
+      // first tile column this warp loads for chunk c, and its TMEM column
+      auto warp_col = [&](int c) { return mode_a ? c * CK : (mode_c ? c * ccols + h * CK : h * 128 + c * CK); };
+      auto tmem_col = [&](int c) { return mode_a ? h * 128 + c * CK : warp_col(c); };
+      auto have_chunk = [&](int c) { return warp_col(c) < t.n_i && !(args.debug & 128); };
+      const uint32_t t_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::kAccCols);
       uint32_t v[CK];  // TMEM chunk in flight: loaded one chunk ahead of its use
-      if (have_chunk(0)) ptx::tmem_ld_32x32b_x32(t_base, v);
-      if (args.epi_tma) {
-        // ---- TMA store epilogue: TMEM -> registers -> OutT staging laid out
-        // [group][row][128 tokens] (group = token half, or column half for
-        // G = 256) -> one thread scatters each 4 staged rows to their C^T rows
-        // with cp.async.bulk.tensor tile::scatter4 (rows >= n_i go to an
-        // out-of-range row and are dropped; tokens >= M are clipped).  No
-        // global store passes through the LSU, which the gathers need.
-        OutT *stg = reinterpret_cast<OutT *>(sStage);
-        constexpr int kBufElems = 2 * CK * 128;
-        auto issue_chunk = [&](int cc) {
-          const OutT *b = stg + (cc & 1) * kBufElems;
-          for (int g = 0; g < 2; ++g) {
-            if (TB == 256 ? g >= nh : g * 128 + cc * CK >= t.n_i) continue;
-            const int tok0 = m0 + (TB == 256 ? g * 128 : 0);
-            const int cbase = (TB == 256 ? 0 : g * 128) + cc * CK;
-            for (int r4 = 0; r4 < CK && cbase + r4 < t.n_i; r4 += 4) {
-              int32_t rows[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) rows[i] = cbase + r4 + i < t.n_i ? ucol[cbase + r4 + i] : args.n_rows;
-              if (!(args.debug & 2)) ptx::tma_scatter4(&args.out_map, tok0, rows, b + (g * CK + r4) * 128);
-            }
-          }
-          ptx::bulk_commit();
-        };
-        for (int ci = 0; ci < n_chunks; ++ci) {
-          const bool have = have_chunk(ci);
-          if (have) ptx::tmem_ld_wait();
-          if (ci == n_chunks - 1) {
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[acc]);
-          }
-          if (issuer) ptx::bulk_wait_read<0>();  // chunk ci - 2 (same buffer) has left smem
-          epi_sync();                            // buffer ci & 1 free; chunk ci - 1 staged
-          if (issuer && ci > 0) issue_chunk(ci - 1);
-          if (have) {
-            OutT *dst = stg + (ci & 1) * kBufElems + h * CK * 128 + q * 32 + lane;
-#pragma unroll
-            for (int jj = 0; jj < CK; ++jj) dst[jj * 128] = cvt_out<OutT>(__uint_as_float(v[jj]));
-            ptx::fence_proxy_async_smem();  // staged data is read by TMA (async proxy)
-          }
-          if (ci + 1 < n_chunks && have_chunk(ci + 1)) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)((ci + 1) * CK), v);
-          if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 3);
-        }
-        epi_sync();  // last chunk staged
-        if (issuer) issue_chunk(n_chunks - 1);
-      } else
+      if (have_chunk(0)) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)tmem_col(0), v);
       for (int ci = 0; ci < n_chunks; ++ci) {
-        const int c0 = ci * CK;
         float *buf = sStage + (ci & 1) * (C::kStageBytes / 4);  // double-buffered staging
-        // 1) TMEM -> registers -> staging buffer [col][token] (conflict-free)
+        // 1) TMEM -> registers -> staging: mode A [32 cols][256 tok], modes
+        //    B/C [h][32 cols][128 tok] (conflict-free: consecutive tokens)
         const bool have = have_chunk(ci);
         if (have) {
           ptx::tmem_ld_wait();
           if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 0);
-          const int tok = (TB == 256 ? h * 128 : 0) + q * 32 + lane;
-          float *dst = buf + (TB == 256 ? 0 : h * CK * TB) + tok;
+          float *dst = mode_a ? buf + h * 128 + q * 32 + lane : buf + h * CK * 128 + q * 32 + lane;
+          const int rs = mode_a ? 256 : 128;
 #pragma unroll
-          for (int jj = 0; jj < CK; ++jj) dst[jj * TB] = __uint_as_float(v[jj]);
+          for (int jj = 0; jj < CK; ++jj) dst[jj * rs] = __uint_as_float(v[jj]);
         }
         if (ci == n_chunks - 1) {
           // all of this warp's TMEM reads for the unit are done: hand the
@@ -547,67 +554,18 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         // whose buffer chunk ci + 1 will overwrite.
         epi_sync();
         // next chunk's TMEM load overlaps this chunk's global stores
-        if (ci + 1 < n_chunks && have_chunk(ci + 1)) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)(c0 + CK), v);
+        if (ci + 1 < n_chunks && have_chunk(ci + 1)) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)tmem_col(ci + 1), v);
         if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 2);
-        // 2) staged rows -> global, one C^T row segment at a time.  All of
-        // this warp's shared-memory reads are issued before its first global
-        // store: an LDS queued behind a backpressured STG in the same pipe
-        // would wait for it, serializing the loop at DRAM-queue latency.
-        constexpr int kRows = C::kStageCols;              // 32 (TB=256) | 64 (TB=128)
-        constexpr int kRowsPerWarp = kRows / kEpiWarps;   // 4 | 8
-        constexpr int NIT = (TB / V + 31) / 32;           // 16-byte pieces per lane per row
-        constexpr int kBatch = kRowsPerWarp * NIT * V > 32 ? 32 / (NIT * V) : kRowsPerWarp;  // rows per load batch
-#pragma unroll
-        for (int r0 = 0; r0 < kRowsPerWarp; r0 += kBatch) {
-          float vals[kBatch][NIT][V];
-          int orows[kBatch];
-#pragma unroll
-          for (int rb = 0; rb < kBatch; ++rb) {
-            const int srow = e * kRowsPerWarp + r0 + rb;
-            const int col = TB == 256 ? c0 + srow : (srow < CK ? c0 + srow : 128 + c0 + (srow - CK));
-            orows[rb] = (col < t.n_i && !(args.debug & 2)) ? ucol[col] : -1;
-            const float *srow_p = buf + srow * TB;
-#pragma unroll
-            for (int n = 0; n < NIT; ++n) {
-              const int tk = (n * 32 + lane) * V;
-#pragma unroll
-              for (int x = 0; x < V; x += 4) {
-                const float4 f =
-                    tk < seg ? *reinterpret_cast<const float4 *>(srow_p + tk + x) : make_float4(0.f, 0.f, 0.f, 0.f);
-                vals[rb][n][x] = f.x; vals[rb][n][x + 1] = f.y; vals[rb][n][x + 2] = f.z; vals[rb][n][x + 3] = f.w;
-              }
-            }
-          }
-#pragma unroll
-          for (int rb = 0; rb < kBatch; ++rb) {
-            if (orows[rb] < 0) continue;
-            OutT *grow = out + (int64_t)orows[rb] * args.ldc + m0;
-#pragma unroll
-            for (int n = 0; n < NIT; ++n) {
-              const int tk = (n * 32 + lane) * V;
-              if (tk >= seg) continue;
-              float *v = vals[rb][n];
-              if (vec && m0 + tk + V <= args.M) {
-                uint4 *p = reinterpret_cast<uint4 *>(grow + tk);
-                if (args.accumulate) unpack16_add<OutT>(*p, v);
-                const uint4 pk = pack16<OutT>(v);
-                if (args.debug & 16) {  // experiment: staging reads without the global store
-                  if ((pk.x ^ pk.y ^ pk.z ^ pk.w) == 0x7fc00001u) __stcs(p, pk);
-                } else {
-                  __stcs(p, pk);
-                }
-              } else {
-#pragma unroll
-                for (int x = 0; x < V; ++x) {
-                  if (m0 + tk + x < args.M) {
-                    float r = v[x];
-                    if (args.accumulate) r += cvt_in<OutT>(grow[tk + x]);
-                    grow[tk + x] = cvt_out<OutT>(r);
-                  }
-                }
-              }
-            }
-          }
+        // 2) staged rows -> global.  All shared-memory reads of a batch are
+        // issued before its first global store: an LDS queued behind a
+        // backpressured STG in the same pipe would wait for it.
+        if (mode_a) {
+          store_rows<OutT, 4, 256>(args, out, buf, e * 4, lane, m0, 256, [&](int r) { return ci * CK + r; }, ucol,
+                                   t.n_i, vec);
+        } else {
+          store_rows<OutT, 8, 128>(args, out, buf, e * 8, lane, m0, 128,
+                                   [&](int r) { return mode_c ? ci * ccols + r : (r < CK ? 0 : 128) + ci * CK + (r % CK); },
+                                   ucol, t.n_i, vec);
         }
         if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 3);
       }
@@ -615,16 +573,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (args.epi_tma) {
-      if (issuer) {
-        while (zq < z1) tma_zero_group();
-        ptx::bulk_wait<0>();  // all TMA stores performed before the CTA exits
-      }
-    } else {
-      for (; zr < z1; zr += kEpiWarps)
-        zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
-      if (lane == 0) ptx::bulk_wait<0>();  // bulk stores performed (and smem read) before exit
-    }
+    for (; zr < z1; zr += kEpiWarps)
+      zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
+    if (lane == 0) ptx::bulk_wait<0>();  // bulk stores performed (and smem read) before exit
     if (e == 0 && lane == 0) trace_evt(args, 7, 1);  // last zero row issued
   }
 

@@ -11,7 +11,6 @@
 
 #include "tw_b200.h"
 
-#include <cuda.h>          // CUtensorMap (all sources are compiled by nvcc)
 #include <vector_types.h>  // int4
 
 namespace tw {
@@ -78,9 +77,6 @@ int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows,
 
 // Kernel arguments of the persistent TW-GEMM (tw_gemm_sm100.cu).
 struct GemmArgs {
-  // TMA map of the output C^T (dims {M, rows}, box {128 tokens, 1 row}, no
-  // swizzle) for the scatter4 store epilogue; valid iff epi_tma
-  CUtensorMap out_map;
   const TileMeta *tiles;
   const int32_t *kidx;
   const int32_t *colids;
@@ -101,8 +97,6 @@ struct GemmArgs {
   uint32_t idesc;     // instruction descriptor without the N field
   int32_t block_n;
   int64_t *trace;     // optional per-CTA event timeline (tw_gemm_traced), else null
-  int32_t epi_tma;    // 1: epilogue + zero rows stored by TMA scatter4 (out_map)
-  int32_t n_rows;     // output rows (OOB row coordinate for masked scatter lanes)
   int32_t zero_policy; // when the epilogue writes zero rows (kernel comment); env TW_B200_ZERO
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };

@@ -95,17 +95,6 @@ __device__ __forceinline__ void cp_async_16(void *smem_dst, const void *gsrc, ui
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(src_bytes)
                : "memory");
 }
-// TMA tile::scatter4 store: 4 rows (rows[0..3], out-of-range rows are
-// skipped) x box-width elements starting at column c0, from 4 consecutive
-// box rows in shared memory
-__device__ __forceinline__ void tma_scatter4(const CUtensorMap *m, int32_t c0, const int32_t (&rows)[4],
-                                             const void *smem_src) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
-          reinterpret_cast<uint64_t>(m)),
-      "r"(c0), "r"(rows[0]), "r"(rows[1]), "r"(rows[2]), "r"(rows[3]), "r"(smem_u32(smem_src))
-      : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until at most N bulk groups still READ shared memory
 template <int N>
