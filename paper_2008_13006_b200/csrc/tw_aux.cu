@@ -3,6 +3,8 @@
 //   spmm   : K3, TEW residual CSC SpMM into C^T rows            (engine.py:167-181,
 //            _kernels.py:30-41), fp32 mul-then-add in ascending p
 //   exact  : bit-exact CUDA-core TW GEMM over a packed plan      (_kernels.py:13-27)
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -60,43 +62,272 @@ __global__ void __launch_bounds__(256) prep_cast_kernel(const float *__restrict_
 }
 
 // ---------------------------------------------------------------- spmm (K3)
-// One warp per output row j (CSC column j == CSR row of S^T), 4 consecutive
-// tokens per lane (128 per warp).  Each stored entry p contributes
-// v * at[row_idx[p], m] with a separately rounded multiply and add, in
-// ascending p -- the exact operation sequence of spmm_accum.
+// One warp per (output row j, segment of 32*TOK tokens); j is a CSC column of
+// S, i.e. a CSR row of S^T.  Lane l owns TOK = 16/sizeof(AT) consecutive
+// tokens and reads them with one 16-byte load per stored entry.  The warp
+// fetches 32 entries (row index, value) at a time into lanes and broadcasts
+// them with shuffles; four entries' A^T loads are in flight at once.  Each
+// entry p contributes v * at[row_idx[p], m] with a separately rounded
+// multiply and add, in ascending p -- the exact operation sequence of
+// spmm_accum (_kernels.py:30-41).
+template <typename AT>
+struct Vec16 {
+  static constexpr int N = 16 / (int)sizeof(AT);
+  __device__ __forceinline__ static void load(const AT *p, float (&o)[N]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4 *>(p));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    if constexpr (sizeof(AT) == 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = __uint_as_float(w[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint16_t b = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
+        o[i] = to_f<AT>(*reinterpret_cast<const AT *>(&b));
+      }
+    }
+  }
+};
+
 template <typename AT, typename OutT>
 __global__ void __launch_bounds__(256) spmm_csc_kernel(const AT *__restrict__ at, int64_t m, int64_t lda,
                                                        int64_t col_begin, int64_t n_cols,
                                                        const int32_t *__restrict__ col_ptr,
                                                        const int32_t *__restrict__ row_idx,
                                                        const float *__restrict__ values, OutT *__restrict__ ct,
-                                                       int64_t ldc, int accumulate) {
+                                                       int64_t ldc, int accumulate, int vec_ok) {
+  constexpr int TOK = Vec16<AT>::N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t jr = (int64_t)blockIdx.y * 8 + warp;  // output row (re-based)
   if (jr >= n_cols) return;
   const int64_t j = jr + col_begin;
-  const int64_t mbase = (int64_t)blockIdx.x * 128 + lane * 4;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  const int p0 = __ldg(col_ptr + j), p1 = __ldg(col_ptr + j + 1);
-  for (int p = p0; p < p1; ++p) {
-    const int64_t kr = __ldg(row_idx + p);
-    const float v = __ldg(values + p);
-    const AT *arow = at + kr * lda;
+  const int64_t mbase = (int64_t)blockIdx.x * (32 * TOK) + lane * TOK;
+  const bool full = vec_ok && mbase + TOK <= m;
+  float acc[TOK];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t mm = mbase + e;
-      if (mm < m) acc[e] = __fadd_rn(acc[e], __fmul_rn(v, to_f<AT>(arow[mm])));
+  for (int x = 0; x < TOK; ++x) acc[x] = 0.f;
+  const int p0 = __ldg(col_ptr + j), p1 = __ldg(col_ptr + j + 1);
+  for (int pb = p0; pb < p1; pb += 32) {
+    const int nb = min(32, p1 - pb);
+    const int my_r = lane < nb ? __ldg(row_idx + pb + lane) : 0;
+    const float my_v = lane < nb ? __ldg(values + pb + lane) : 0.f;
+    int e = 0;
+    for (; e + 4 <= nb; e += 4) {
+      float a[4][TOK];
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t kr = __shfl_sync(0xffffffffu, my_r, e + u);
+        v[u] = __shfl_sync(0xffffffffu, my_v, e + u);
+        const AT *ap = at + kr * lda + mbase;
+        if (full) {
+          Vec16<AT>::load(ap, a[u]);
+        } else {
+#pragma unroll
+          for (int x = 0; x < TOK; ++x) a[u][x] = mbase + x < m ? to_f<AT>(ap[x]) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int x = 0; x < TOK; ++x) acc[x] = __fadd_rn(acc[x], __fmul_rn(v[u], a[u][x]));
+    }
+    for (; e < nb; ++e) {
+      const int64_t kr = __shfl_sync(0xffffffffu, my_r, e);
+      const float v = __shfl_sync(0xffffffffu, my_v, e);
+      const AT *ap = at + kr * lda + mbase;
+      float a[TOK];
+      if (full) {
+        Vec16<AT>::load(ap, a);
+      } else {
+#pragma unroll
+        for (int x = 0; x < TOK; ++x) a[x] = mbase + x < m ? to_f<AT>(ap[x]) : 0.f;
+      }
+#pragma unroll
+      for (int x = 0; x < TOK; ++x) acc[x] = __fadd_rn(acc[x], __fmul_rn(v, a[x]));
     }
   }
   OutT *crow = ct + jr * ldc;
+  constexpr int OV = 16 / (int)sizeof(OutT);  // outputs per 16-byte store
+  if (full && (vec_ok & 2) && TOK % OV == 0) {
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int64_t mm = mbase + e;
+    for (int x0 = 0; x0 < TOK; x0 += OV) {
+      uint4 *p = reinterpret_cast<uint4 *>(crow + mbase + x0);
+      float r[OV];
+#pragma unroll
+      for (int x = 0; x < OV; ++x) r[x] = acc[x0 + x];
+      if (accumulate) {
+        const uint4 old = *p;
+        const uint32_t w[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+        for (int x = 0; x < OV; ++x) {
+          float o;
+          if constexpr (sizeof(OutT) == 4) {
+            o = __uint_as_float(w[x]);
+          } else {
+            const uint16_t bits = (uint16_t)(w[x >> 1] >> ((x & 1) * 16));
+            o = to_f<OutT>(*reinterpret_cast<const OutT *>(&bits));
+          }
+          r[x] = __fadd_rn(o, r[x]);
+        }
+      }
+      uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int x = 0; x < OV; ++x) {
+        if constexpr (sizeof(OutT) == 4) {
+          w[x] = __float_as_uint(r[x]);
+        } else {
+          OutT o = to_t<OutT>(r[x]);
+          w[x >> 1] |= (uint32_t)(*reinterpret_cast<uint16_t *>(&o)) << ((x & 1) * 16);
+        }
+      }
+      *p = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int x = 0; x < TOK; ++x) {
+    const int64_t mm = mbase + x;
     if (mm < m) {
-      float r = acc[e];
+      float r = acc[x];
       if (accumulate) r = __fadd_rn(to_f<OutT>(crow[mm]), r);
       crow[mm] = to_t<OutT>(r);
     }
+  }
+}
+
+// PER consecutive activations from shared memory as fp32 (one vector load)
+template <typename AT, int PER>
+__device__ __forceinline__ void load_smem_vec(const AT *p, float (&o)[PER]) {
+  if constexpr (sizeof(AT) == 2 && PER == 4) {
+    const uint2 u = *reinterpret_cast<const uint2 *>(p);
+    const uint32_t w[2] = {u.x, u.y};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint16_t b = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
+      o[i] = to_f<AT>(*reinterpret_cast<const AT *>(&b));
+    }
+  } else if constexpr (sizeof(AT) == 4 && PER == 4) {
+    const float4 f = *reinterpret_cast<const float4 *>(p);
+    o[0] = f.x; o[1] = f.y; o[2] = f.z; o[3] = f.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) o[i] = to_f<AT>(p[i]);
+  }
+}
+// PER consecutive outputs of row `crow` from token mt (accumulating if asked)
+template <typename OutT, int PER>
+__device__ __forceinline__ void store_vec(OutT *crow, int64_t mt, int64_t m, const float (&acc)[PER], int accumulate) {
+#pragma unroll
+  for (int x = 0; x < PER; ++x) {
+    const int64_t mm = mt + x;
+    if (mm < m) {
+      float r = acc[x];
+      if (accumulate) r = __fadd_rn(to_f<OutT>(crow[mm]), r);
+      crow[mm] = to_t<OutT>(r);
+    }
+  }
+}
+
+// Shared-memory tiled variant (K3, default): the CTA copies the whole A^T
+// token segment at[0:K, m0:m0+T] into shared memory once (cp.async), then
+// its 8 warps walk columns j0, j0+1, ... of its column group: warp = column,
+// lane = T/32 consecutive tokens, every stored entry read from smem.  A^T is
+// read from L2 once per (segment, column group) instead of once per stored
+// entry -- 2*nnz*M bytes of L2 traffic become ~groups*2*K*M.  Same exact
+// multiply-then-add sequence in ascending p.
+constexpr int kSpmmWarps = 16;
+template <typename AT, typename OutT, int T>
+__global__ void __launch_bounds__(kSpmmWarps * 32) spmm_tiled_kernel(const AT *__restrict__ at, int64_t m, int64_t k, int64_t lda,
+                                                         int64_t col_begin, int64_t n_cols, int cols_per_cta,
+                                                         const int32_t *__restrict__ col_ptr,
+                                                         const int32_t *__restrict__ row_idx,
+                                                         const float *__restrict__ values, OutT *__restrict__ ct,
+                                                         int64_t ldc, int accumulate, int64_t smem_bytes) {
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  AT *sa = reinterpret_cast<AT *>(sm_raw);  // [K][T]
+  constexpr int RB = T * (int)sizeof(AT);   // bytes per staged row
+  constexpr int CPR = RB / 16;              // 16-byte chunks per row
+  constexpr int PER = T / 32;               // tokens per lane
+  const int64_t m0 = (int64_t)blockIdx.x * T;
+  const int64_t j0 = (int64_t)blockIdx.y * cols_per_cta;
+  const int64_t j1 = min(n_cols, j0 + cols_per_cta);
+  // stage A^T[0:K, m0:m0+T] (zero-filled past M)
+  for (int64_t c = threadIdx.x; c < k * CPR; c += blockDim.x) {
+    const int64_t r = c / CPR, cc = c % CPR;
+    const int64_t tok = m0 + cc * (16 / (int)sizeof(AT));
+    const int64_t avail = m - tok;
+    const uint32_t nbytes = avail >= 16 / (int)sizeof(AT) ? 16u : (avail > 0 ? (uint32_t)(avail * sizeof(AT)) : 0u);
+    const AT *src = nbytes ? at + r * lda + tok : at;
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm_raw + r * RB + cc * 16);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(nbytes) : "memory");
+  }
+  // The column group's CSC slice (pointers, rows, values) is staged in the
+  // shared memory left after the A^T segment when it fits; every warp then
+  // reads its entries with broadcast shared loads instead of global loads
+  // whose latency would sit on each column's critical path.
+  const int64_t pg0 = __ldg(col_ptr + j0 + col_begin), pg1 = __ldg(col_ptr + j1 + col_begin);
+  const int64_t ncg = j1 - j0;
+  int32_t *s_ptr = reinterpret_cast<int32_t *>(sm_raw + k * RB);
+  int32_t *s_row = s_ptr + ncg + 1;
+  float *s_val = reinterpret_cast<float *>(s_row + (pg1 - pg0));
+  const bool staged = (int64_t)(k * RB) + (ncg + 1 + 2 * (pg1 - pg0)) * 4 <= smem_bytes;
+  if (staged) {
+    for (int64_t i = threadIdx.x; i <= ncg; i += blockDim.x) s_ptr[i] = __ldg(col_ptr + j0 + col_begin + i) - (int32_t)pg0;
+    for (int64_t i = threadIdx.x; i < pg1 - pg0; i += blockDim.x) {
+      s_row[i] = __ldg(row_idx + pg0 + i);
+      s_val[i] = __ldg(values + pg0 + i);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t mt = m0 + lane * PER;
+  for (int64_t jr = j0 + warp; jr < j1; jr += kSpmmWarps) {
+    float acc[PER];
+#pragma unroll
+    for (int x = 0; x < PER; ++x) acc[x] = 0.f;
+    if (staged) {
+      const int q0 = s_ptr[jr - j0], q1 = s_ptr[jr - j0 + 1];
+      int q = q0;
+      for (; q + 4 <= q1; q += 4) {  // four entries' loads in flight, adds still in order
+        float a[4][PER], v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = s_val[q + u];
+          load_smem_vec<AT, PER>(sa + (int64_t)s_row[q + u] * T + lane * PER, a[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int x = 0; x < PER; ++x) acc[x] = __fadd_rn(acc[x], __fmul_rn(v[u], a[u][x]));
+      }
+      for (; q < q1; ++q) {
+        float a[PER];
+        const float v = s_val[q];
+        load_smem_vec<AT, PER>(sa + (int64_t)s_row[q] * T + lane * PER, a);
+#pragma unroll
+        for (int x = 0; x < PER; ++x) acc[x] = __fadd_rn(acc[x], __fmul_rn(v, a[x]));
+      }
+    } else {
+      const int64_t j = jr + col_begin;
+      const int p0 = __ldg(col_ptr + j), p1 = __ldg(col_ptr + j + 1);
+      for (int pb = p0; pb < p1; pb += 32) {
+        const int nb = min(32, p1 - pb);
+        const int my_r = lane < nb ? __ldg(row_idx + pb + lane) : 0;
+        const float my_v = lane < nb ? __ldg(values + pb + lane) : 0.f;
+        for (int e = 0; e < nb; ++e) {
+          const int r = __shfl_sync(0xffffffffu, my_r, e);
+          const float v = __shfl_sync(0xffffffffu, my_v, e);
+          float a[PER];
+          load_smem_vec<AT, PER>(sa + (int64_t)r * T + lane * PER, a);
+#pragma unroll
+          for (int x = 0; x < PER; ++x) acc[x] = __fadd_rn(acc[x], __fmul_rn(v, a[x]));
+        }
+      }
+    }
+    store_vec<OutT, PER>(ct + jr * ldc, mt, m, acc, accumulate);
   }
 }
 
@@ -172,23 +403,61 @@ cudaError_t prep_t(const float *a, int64_t m, int64_t k, int layout, T *at, int6
   return cudaGetLastError();
 }
 
+template <typename AT, typename OutT, int T>
+cudaError_t spmm_tiled(const void *at, int64_t m, int64_t k, int64_t lda, int64_t col_begin, int64_t n_cols,
+                       const int32_t *cp, const int32_t *ri, const float *va, void *ct, int64_t ldc, int accumulate,
+                       cudaStream_t s) {
+  // A^T segment + room for the column group's CSC slice (up to the 227 KB limit)
+  const int smem = 232448;
+  auto kern = spmm_tiled_kernel<AT, OutT, T>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t segs = (m + T - 1) / T;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  // enough CTAs for ~2 waves, as few column groups (A^T re-reads) as that allows
+  const int64_t groups =
+      std::max<int64_t>(1, std::min<int64_t>((n_cols + kSpmmWarps - 1) / kSpmmWarps, (2 * sms + segs - 1) / segs));
+  const int cpc = (int)((n_cols + groups - 1) / groups);
+  dim3 grid((unsigned)segs, (unsigned)((n_cols + cpc - 1) / cpc));
+  kern<<<grid, kSpmmWarps * 32, smem, s>>>(reinterpret_cast<const AT *>(at), m, k, lda, col_begin, n_cols, cpc, cp, ri, va,
+                               reinterpret_cast<OutT *>(ct), ldc, accumulate, (int64_t)smem);
+  return cudaGetLastError();
+}
+
 template <typename AT, typename OutT>
-cudaError_t spmm_t(const void *at, int64_t m, int64_t lda, int64_t col_begin, int64_t n_cols, const int32_t *cp,
-                   const int32_t *ri, const float *va, void *ct, int64_t ldc, int accumulate, cudaStream_t s) {
-  dim3 grid((unsigned)((m + 127) / 128), (unsigned)((n_cols + 7) / 8));
+cudaError_t spmm_t(const void *at, int64_t m, int64_t k, int64_t lda, int64_t col_begin, int64_t n_cols,
+                   const int32_t *cp, const int32_t *ri, const float *va, void *ct, int64_t ldc, int accumulate,
+                   cudaStream_t s) {
+  // tiled (shared-memory) kernel when a T >= 32 token segment of all K rows fits
+  constexpr int64_t kMaxSmem = 200 * 1024;
+  const bool al = (reinterpret_cast<uintptr_t>(at) & 15) == 0 && (lda * (int64_t)sizeof(AT)) % 16 == 0;
+  if (al && k > 0) {
+    if (k * 128 * (int64_t)sizeof(AT) <= kMaxSmem)
+      return spmm_tiled<AT, OutT, 128>(at, m, k, lda, col_begin, n_cols, cp, ri, va, ct, ldc, accumulate, s);
+    if (k * 64 * (int64_t)sizeof(AT) <= kMaxSmem)
+      return spmm_tiled<AT, OutT, 64>(at, m, k, lda, col_begin, n_cols, cp, ri, va, ct, ldc, accumulate, s);
+    if (k * 32 * (int64_t)sizeof(AT) <= kMaxSmem)
+      return spmm_tiled<AT, OutT, 32>(at, m, k, lda, col_begin, n_cols, cp, ri, va, ct, ldc, accumulate, s);
+  }
+  constexpr int seg = 32 * (16 / (int)sizeof(AT));
+  // bit 0: 16-byte activation loads; bit 1: 16-byte output stores
+  const int vec_ok = (((reinterpret_cast<uintptr_t>(at) & 15) == 0) && ((lda * (int64_t)sizeof(AT)) % 16 == 0) ? 1 : 0) |
+                     (((reinterpret_cast<uintptr_t>(ct) & 15) == 0) && ((ldc * (int64_t)sizeof(OutT)) % 16 == 0) ? 2 : 0);
+  dim3 grid((unsigned)((m + seg - 1) / seg), (unsigned)((n_cols + 7) / 8));
   spmm_csc_kernel<AT, OutT><<<grid, 256, 0, s>>>(reinterpret_cast<const AT *>(at), m, lda, col_begin, n_cols, cp, ri,
-                                                  va, reinterpret_cast<OutT *>(ct), ldc, accumulate);
+                                                  va, reinterpret_cast<OutT *>(ct), ldc, accumulate, vec_ok);
   return cudaGetLastError();
 }
 
 template <typename AT>
-cudaError_t spmm_at(const void *at, int64_t m, int64_t lda, int64_t cb, int64_t nc, const int32_t *cp,
+cudaError_t spmm_at(const void *at, int64_t m, int64_t k, int64_t lda, int64_t cb, int64_t nc, const int32_t *cp,
                     const int32_t *ri, const float *va, void *ct, int64_t ldc, int out_dtype, int acc,
                     cudaStream_t s) {
   switch (out_dtype) {
-    case TW_F32: return spmm_t<AT, float>(at, m, lda, cb, nc, cp, ri, va, ct, ldc, acc, s);
-    case TW_BF16: return spmm_t<AT, __nv_bfloat16>(at, m, lda, cb, nc, cp, ri, va, ct, ldc, acc, s);
-    case TW_F16: return spmm_t<AT, __half>(at, m, lda, cb, nc, cp, ri, va, ct, ldc, acc, s);
+    case TW_F32: return spmm_t<AT, float>(at, m, k, lda, cb, nc, cp, ri, va, ct, ldc, acc, s);
+    case TW_BF16: return spmm_t<AT, __nv_bfloat16>(at, m, k, lda, cb, nc, cp, ri, va, ct, ldc, acc, s);
+    case TW_F16: return spmm_t<AT, __half>(at, m, k, lda, cb, nc, cp, ri, va, ct, ldc, acc, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -205,14 +474,14 @@ cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t lda, int64_t col_begin, int64_t n_cols,
+cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t k, int64_t lda, int64_t col_begin, int64_t n_cols,
                         const int32_t *cp, const int32_t *ri, const float *va, void *ct, int64_t ldc, int out_dtype,
                         int accumulate, cudaStream_t s) {
   switch (at_dtype) {
-    case TW_F32: return spmm_at<float>(at, m, lda, col_begin, n_cols, cp, ri, va, ct, ldc, out_dtype, accumulate, s);
+    case TW_F32: return spmm_at<float>(at, m, k, lda, col_begin, n_cols, cp, ri, va, ct, ldc, out_dtype, accumulate, s);
     case TW_BF16:
-      return spmm_at<__nv_bfloat16>(at, m, lda, col_begin, n_cols, cp, ri, va, ct, ldc, out_dtype, accumulate, s);
-    case TW_F16: return spmm_at<__half>(at, m, lda, col_begin, n_cols, cp, ri, va, ct, ldc, out_dtype, accumulate, s);
+      return spmm_at<__nv_bfloat16>(at, m, k, lda, col_begin, n_cols, cp, ri, va, ct, ldc, out_dtype, accumulate, s);
+    case TW_F16: return spmm_at<__half>(at, m, k, lda, col_begin, n_cols, cp, ri, va, ct, ldc, out_dtype, accumulate, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -14,7 +14,7 @@ int tokens_per_unit(int block_n);
 cudaError_t launch_tw_gemm_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream);
 cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
                         cudaStream_t s);
-cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t lda, int64_t col_begin, int64_t n_cols,
+cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t k, int64_t lda, int64_t col_begin, int64_t n_cols,
                         const int32_t *cp, const int32_t *ri, const float *va, void *ct, int64_t ldc, int out_dtype,
                         int accumulate, cudaStream_t s);
 cudaError_t launch_exact(const tw_plan *p, const float *at, int64_t m, int64_t lda, float *ct, int64_t ldc,
@@ -293,13 +293,12 @@ int tw_spmm_csc(const void *at, int at_dtype, int64_t k, int64_t m, int64_t lda,
                 const int32_t *row_idx, const float *values, void *ct, int64_t ldc, int out_dtype, int accumulate,
                 void *stream) {
   clear_error();
-  (void)k;
   if (m < 0 || n < 0 || lda < m || ldc < m) return fail(TW_ERR_DIMENSION, "bad M / N / lda / ldc");
   if (m == 0 || n == 0) return TW_OK;
   int sms = 0;
   int rc = require_sm100(&sms);
   if (rc) return rc;
-  cudaError_t e = launch_spmm(at, at_dtype, m, lda, 0, n, col_ptr, row_idx, values, ct, ldc, out_dtype, accumulate,
+  cudaError_t e = launch_spmm(at, at_dtype, m, k, lda, 0, n, col_ptr, row_idx, values, ct, ldc, out_dtype, accumulate,
                               reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tw_spmm_csc launch");
   return TW_OK;
@@ -320,7 +319,7 @@ int tw_gemm_tew(const tw_plan *p, const void *at, int64_t m, int64_t lda, const 
   if (rc) return rc;
   // SpMM writes every row of the plan's column range (overlay covers pruned
   // columns too, pruning.py:548-549); the TW kernel then adds into kept rows.
-  cudaError_t e = launch_spmm(at, hp.in_dtype, m, lda, hp.col_begin, hp.col_end - hp.col_begin, col_ptr, row_idx,
+  cudaError_t e = launch_spmm(at, hp.in_dtype, m, hp.k, lda, hp.col_begin, hp.col_end - hp.col_begin, col_ptr, row_idx,
                               values, ct, ldc, out_dtype, 0, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tw_gemm_tew spmm launch");
   return tw_gemm(p, at, m, lda, ct, ldc, out_dtype, 1, stream);
