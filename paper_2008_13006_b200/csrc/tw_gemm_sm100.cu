@@ -32,6 +32,7 @@
 // Warp roles (416 threads): w0-3 producer (A gather + W bulk copy), w4 MMA
 // issuer + TMEM owner, w5-12 epilogue (TMEM lane quadrant = warp % 4).
 #include <cuda.h>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -295,6 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   const int n_st = __ldg(args.stream_off + blockIdx.x + 1) - s_begin;
 
   if (threadIdx.x == 0) trace_evt(args, 7, 0);  // CTA start
+  // Programmatic dependent launch: let the next kernel in the stream start
+  // its CTAs (they wait in griddepcontrol.wait until this grid completes).
+  // This CTA itself only touches immutable plan data (schedule, weights)
+  // until its own griddepcontrol.wait below.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -345,6 +351,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (k < n_st) prefetch(k);
       ptx::cp_async_commit();
     }
+    // A^T may be produced by the previous kernel in the stream (PDL)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int i = 0; i < n_st; ++i) {
       const int32_t *slot = ring + (i % kIdxSlots) * kSlotInts;
       const long long c0 = clock64();
@@ -492,6 +500,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // bulk stores) while it waits for an accumulator (policy 0: any unit; 1:
     // the CTA's last unit only; 2: none), and the rest at the end
     int zr = __ldg(args.zero_off + blockIdx.x) + e;
+    // the output may be read / written by the previous kernel (PDL)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int z1 = (args.accumulate || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
     constexpr int CK = C::kChunk;              // 32 accumulator columns per TMEM load
     int acc = 0;
@@ -592,7 +602,24 @@ cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
   const int smem = (int)Cfg<BN>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads, smem, stream>>>(args);
+  // programmatic dependent launch (TW_B200_PDL=0 disables): the next grid's
+  // CTAs may start as SMs free up; griddepcontrol.wait orders memory
+  static const bool pdl = [] {
+    const char *e = std::getenv("TW_B200_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, kern, args);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
