@@ -499,7 +499,13 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... (8 KB TMA
     // bulk stores) while it waits for an accumulator (policy 0: any unit; 1:
     // the CTA's last unit only; 2: none), and the rest at the end
-    int zr = __ldg(args.zero_off + blockIdx.x) + e;
+    // Zero rows: while units are in flight only warp 0 writes them, with at
+    // most 3 bulk stores in flight -- the TMA engine also carries the
+    // producer's weight loads, and a burst of zero-row stores queued ahead
+    // of them stalls the pipeline; the remainder is split over all 8 warps
+    // once the CTA's last accumulator has been drained.
+    int zr = __ldg(args.zero_off + blockIdx.x);
+    volatile int32_t *s_zdone = reinterpret_cast<volatile int32_t *>(tmem_holder + 1);
     // the output may be read / written by the previous kernel (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int z1 = (args.accumulate || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
@@ -520,9 +526,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       // (non-blocking test_wait while there is filler work: try_wait would
       // suspend the warp for up to its time limit between zero rows)
       const bool fill = args.zero_policy == 0 || (args.zero_policy == 1 && j == u_end - 1);
-      while (fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
+      while (e == 0 && fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
+        if (lane == 0 && bulk_ok) ptx::bulk_wait_read<2>();
         zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
-        zr += kEpiWarps;
+        ++zr;
       }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
@@ -583,7 +590,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    for (; zr < z1; zr += kEpiWarps)
+    if (e == 0 && lane == 0) *s_zdone = zr;
+    epi_sync();
+    for (zr = *s_zdone + e; zr < z1; zr += kEpiWarps)
       zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
     if (lane == 0) ptx::bulk_wait<0>();  // bulk stores performed (and smem read) before exit
     if (e == 0 && lane == 0) trace_evt(args, 7, 1);  // last zero row issued
