@@ -33,6 +33,7 @@
 // issuer + TMEM owner, w5-12 epilogue (TMEM lane quadrant = warp % 4).
 #include <cuda.h>
 #include <cstdlib>
+#include <type_traits>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -114,14 +115,20 @@ __device__ __forceinline__ uint4 pack16(const float *v) {
   if constexpr (sizeof(OutT) == 4) {
     r = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
   } else {
-    uint16_t h[8];
+    // paired conversions (one F2FP.PACK_AB per two values; the scalar
+    // F2F.F16.F32 form is a low-throughput instruction on the epilogue path)
+    uint32_t w[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      OutT o = cvt_out<OutT>(v[i]);
-      h[i] = *reinterpret_cast<uint16_t *>(&o);
+    for (int i = 0; i < 4; ++i) {
+      if constexpr (std::is_same<OutT, __half>::value) {
+        const __half2 p = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t *>(&p);
+      } else {
+        const __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t *>(&p);
+      }
     }
-    r = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16), h[4] | (uint32_t(h[5]) << 16),
-                   h[6] | (uint32_t(h[7]) << 16));
+    r = make_uint4(w[0], w[1], w[2], w[3]);
   }
   return r;
 }
