@@ -91,17 +91,27 @@ class PackedPlan:
 
     _create = "tw_plan_build_host"
 
-    def __init__(self, tiles: CompactTileSet, dtype: str = "bf16", col_range=None):
+    def __init__(self, tiles: CompactTileSet, dtype: str = "bf16", col_range=None, _arrays=None):
         self._h = None
-        k, n, g, c0, c1, col_off, col_ids, words, subs, sub_off = _plan_args(tiles, col_range)
+        if _arrays is not None:  # packer arrays straight from a file (formats.plan_from_files)
+            k, n, g, col_off, col_ids, words, subs, sub_off = _arrays
+            c0, c1 = col_range if col_range is not None else (0, n)
+            n_tiles = len(col_off) - 1
+        else:
+            k, n, g, c0, c1, col_off, col_ids, words, subs, sub_off = _plan_args(tiles, col_range)
+            n_tiles = len(tiles.tiles)
         self.k, self.n, self.g, self.col_begin, self.col_end = k, n, g, c0, c1
         self.in_code = {"bf16": _lib.TW_BF16, "fp16": _lib.TW_F16}[dtype]
         handle = ctypes.c_void_p()
-        self._build(handle, k, n, g, len(tiles.tiles), col_off, col_ids, words, subs, sub_off, c0, c1)
+        self._build(handle, k, n, g, n_tiles, col_off, col_ids, words, subs, sub_off, c0, c1)
         self._h = handle
         info = _lib.PlanInfo()
         _lib.call("tw_plan_get_info", self._h, ctypes.byref(info))
         self.info = {f: getattr(info, f) for f, _ in _lib.PlanInfo._fields_}
+
+    @classmethod
+    def _host_from_arrays(cls, k, n, g, col_off, col_ids, words, subs, sub_off, dtype="bf16", col_range=None):
+        return PackedPlan(None, dtype, col_range, (int(k), int(n), int(g), col_off, col_ids, words, subs, sub_off))
 
     def _build(self, handle, k, n, g, nt, col_off, col_ids, words, subs, sub_off, c0, c1):
         _lib.call(self._create, k, n, g, nt, _np_ptr(col_off), _np_ptr(col_ids), _np_ptr(words), _np_ptr(subs),
@@ -163,7 +173,7 @@ class TwPlan(PackedPlan):
 
     _create = "tw_plan_create"
 
-    def __init__(self, tiles: CompactTileSet, device=None, dtype=None, col_range=None):
+    def __init__(self, tiles: CompactTileSet, device=None, dtype=None, col_range=None, _arrays=None):
         if torch is None:
             raise RuntimeError("torch is required for device plans")
         dtype = dtype or torch.bfloat16
@@ -171,7 +181,12 @@ class TwPlan(PackedPlan):
             raise ValueError("plan dtype must be bfloat16 or float16")
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        super().__init__(tiles, "bf16" if dtype == torch.bfloat16 else "fp16", col_range)
+        super().__init__(tiles, "bf16" if dtype == torch.bfloat16 else "fp16", col_range, _arrays)
+
+    @classmethod
+    def _from_arrays(cls, k, n, g, col_off, col_ids, words, subs, sub_off, device=None, dtype=None, col_range=None):
+        return cls(None, device=device, dtype=dtype, col_range=col_range,
+                   _arrays=(int(k), int(n), int(g), col_off, col_ids, words, subs, sub_off))
 
     def _build(self, *args):
         with torch.cuda.device(self.device):
