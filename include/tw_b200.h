@@ -160,6 +160,14 @@ int tw_schedule_export(const tw_plan *plan, int64_t m, int out_dtype, int accumu
 int tw_gemm(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
             int out_dtype, int accumulate, void *stream);
 
+/* trainer.py:232-250 engine_logits layer: tw_gemm with the bias + ReLU
+ * epilogue fused -- ct[j, m] = relu?(C[m, j] + bias[j]) for every output
+ * column j of the plan's range, pruned columns included (they become the
+ * constant relu?(bias[j])).  fp32 add then max, rounded once to out_dtype.
+ * bias: DEVICE fp32 array indexed by global output column (length N). */
+int tw_gemm_bias(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
+                 int out_dtype, const float *bias, int relu, void *stream);
+
 /* Bit-exact CUDA-core variant of tw_gemm: fp32 multiply then fp32 add, in
  * ascending k per element (exactly mm_accum's rounding sequence); used to
  * prove layouts/indexing independent of tensor-core accumulation order.

@@ -35,6 +35,7 @@ from .pattern import (
     zero_fill,
 )
 from .sharded import ShardedTwPlan, all_gather_rows, shard_ranges
+from .layers import TwMlp, engine_logits
 from .formats import plan_from_files, read_csc, read_matrix, read_pattern, write_csc, write_matrix, write_pattern
 from .engine import (
     DeviceCsc,

@@ -183,11 +183,20 @@ int tw_plan_destroy(tw_plan *p) {
 }
 
 static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
-                     int out_dtype, int accumulate, int64_t *trace, void *stream);
+                     int out_dtype, int accumulate, int64_t *trace, void *stream, const float *bias = nullptr,
+                     int relu = 0);
 
 int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
             int accumulate, void *stream) {
   return gemm_impl(p, at, m, lda, ct, ldc, out_dtype, accumulate, nullptr, stream);
+}
+
+int tw_gemm_bias(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
+                 const float *bias, int relu, void *stream) {
+  if (!bias) return fail(TW_ERR_ARG, "null bias");
+  if (!p) return fail(TW_ERR_ARG, "null plan");
+  // bias is indexed by global output column; the kernel indexes by plan row
+  return gemm_impl(p, at, m, lda, ct, ldc, out_dtype, 0, nullptr, stream, bias + p->host.col_begin, relu ? 1 : 0);
 }
 
 int tw_gemm_traced(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
@@ -197,7 +206,7 @@ int tw_gemm_traced(const tw_plan *p, const void *at, int64_t m, int64_t lda, voi
 }
 
 static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
-                     int out_dtype, int accumulate, int64_t *trace, void *stream) {
+                     int out_dtype, int accumulate, int64_t *trace, void *stream, const float *bias, int relu) {
   clear_error();
   if (!p) return fail(TW_ERR_ARG, "null plan");
   if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan (tw_plan_build_host) cannot run on the GPU");
@@ -246,6 +255,8 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 15) | ((128u >> 4) << 24);
   a.block_n = hp.block_n;
   a.trace = trace;
+  a.bias = bias;
+  a.relu = relu;
   static const int zero_policy = [] {
     const char *e = std::getenv("TW_B200_ZERO");
     return e ? std::atoi(e) : 0;

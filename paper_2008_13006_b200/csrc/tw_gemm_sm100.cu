@@ -147,16 +147,27 @@ __device__ __forceinline__ void unpack16_add(uint4 old, float *v) {
   }
 }
 
-// One zero row (a pruned column of C) written by one warp: coalesced 16-byte
-// streaming stores, 512 B per instruction.
+// Epilogue value of a pruned output column: 0, or relu?(0 + bias) when the
+// bias/ReLU epilogue is fused (trainer.py:246-248 applies both to every
+// column of the layer output, pruned ones included).
+__device__ __forceinline__ float const_row_value(const GemmArgs &a, int row) {
+  if (a.bias == nullptr) return 0.f;
+  const float b = __fadd_rn(0.f, __ldg(a.bias + row));
+  return a.relu ? fmaxf(b, 0.f) : b;
+}
+
+// One constant row (a pruned column of C) written by one warp: coalesced
+// 16-byte streaming stores, 512 B per instruction.
 template <typename OutT>
 __device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int lane, bool vec) {
   OutT *base = reinterpret_cast<OutT *>(a.out) + (int64_t)row * a.ldc;
   const int64_t n16 = vec ? (int64_t)a.M * (int64_t)sizeof(OutT) / 16 : 0;
   uint4 *b16 = reinterpret_cast<uint4 *>(base);
-  const uint4 z = make_uint4(0, 0, 0, 0);
+  const float c = const_row_value(a, row);
+  float cv[8] = {c, c, c, c, c, c, c, c};
+  const uint4 z = pack16<OutT>(cv);
   for (int64_t i = lane; i < n16; i += 32) __stcs(b16 + i, z);
-  for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(0.f);
+  for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(c);
 }
 
 // One zero row by 1-D TMA bulk stores (up to 8 KB each) from the zeroed smem
@@ -166,7 +177,7 @@ __device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int l
 template <typename OutT>
 __device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int lane, bool bulk_ok, bool vec,
                                               const uint8_t *zero_buf, uint32_t zero_bytes) {
-  if (!bulk_ok) {
+  if (!bulk_ok || (a.bias != nullptr && const_row_value(a, row) != 0.f)) {
     write_zero_row<OutT>(a, row, lane, vec);
     return;
   }
@@ -216,6 +227,16 @@ __device__ __forceinline__ void store_rows(const GemmArgs &args, OutT *out, cons
     for (int rb = 0; rb < kBatch; ++rb) {
       if (orows[rb] < 0) continue;
       OutT *grow = out + (int64_t)orows[rb] * args.ldc + m0;
+      if (args.bias != nullptr) {  // fused bias (+ ReLU): fp32 add then max, as trainer.py:246-248
+        const float bz = __ldg(args.bias + orows[rb]);
+#pragma unroll
+        for (int n = 0; n < NIT; ++n)
+#pragma unroll
+          for (int x = 0; x < V; ++x) {
+            const float z = __fadd_rn(vals[rb][n][x], bz);
+            vals[rb][n][x] = args.relu ? fmaxf(z, 0.f) : z;
+          }
+      }
 #pragma unroll
       for (int n = 0; n < NIT; ++n) {
         const int tk = (n * 32 + lane) * V;

@@ -97,6 +97,8 @@ struct GemmArgs {
   uint32_t idesc;     // instruction descriptor without the N field
   int32_t block_n;
   int64_t *trace;     // optional per-CTA event timeline (tw_gemm_traced), else null
+  const float *bias;  // optional per-output-row bias (fp32, row-rebased), fused epilogue
+  int32_t relu;       // 1: max(x, 0) after the bias (trainer.py:246-248)
   int32_t zero_policy; // when the epilogue writes zero rows (kernel comment); env TW_B200_ZERO
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };

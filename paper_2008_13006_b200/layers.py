@@ -1,0 +1,80 @@
+"""Layer-chaining caller of the TW path: the reference trainer's engine
+forward (trainer.py:232-250 `engine_logits`), on the GPU.
+
+The reference runs, per layer, compact(W) -> gemm_tw -> `+ bias` -> ReLU
+(not after the last layer), copying every activation back to a host
+DenseMatrix.  Here every layer is one persistent TW-GEMM with the bias/ReLU
+epilogue fused, and activations never leave HBM or change layout: a layer's
+output C^T (N x M) is exactly the next layer's A^T (the paper's "transpose
+A only in the first layer, C after the last").  Intermediate
+activations are stored in the plan dtype (fp16 by default: the GEMM operands
+are 16-bit anyway); the last layer writes fp32 logits.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .engine import TwPlan, prep_activations
+from .matrix import DenseMatrix, DimensionError, Layout
+from .pattern import compact
+
+try:
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+
+class TwMlp:
+    """Device-resident TW layers of an MLP: one TwPlan + fp32 bias per layer.
+    `weights` K_i x N_i arrays, `biases` N_i arrays, `patterns` TilePatterns
+    (the reference's MlpModel.weights / .biases and per-layer patterns)."""
+
+    def __init__(self, weights, biases, patterns, device=None, dtype=None):
+        if not (len(weights) == len(biases) == len(patterns)):
+            raise DimensionError("need one pattern per layer")  # trainer.py:239-240
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dtype = dtype or torch.float16
+        self.plans, self.biases = [], []
+        for w, b, p in zip(weights, biases, patterns):
+            ts = compact(DenseMatrix.from_array(np.asarray(w, np.float32)), p)
+            self.plans.append(TwPlan(ts, device=self.device, dtype=self.dtype))
+            bb = np.asarray(b, np.float32).reshape(-1)
+            if bb.size != ts.n:
+                raise DimensionError(f"bias has {bb.size} entries, layer has {ts.n} outputs")
+            self.biases.append(torch.from_numpy(bb).to(self.device))
+        for a, b in zip(self.plans, self.plans[1:]):
+            if a.n != b.k:
+                raise DimensionError(f"layer output {a.n} does not match next layer input {b.k}")
+
+    def forward_t(self, at, stream=None):
+        """A^T (K0 x M, plan dtype) -> logits^T (N_last x M, fp32), all on device."""
+        last = len(self.plans) - 1
+        for i, (plan, b) in enumerate(zip(self.plans, self.biases)):
+            m = at.shape[1]
+            if i < last:
+                ld = (m + 7) // 8 * 8  # next layer gathers 16-byte row chunks
+                out = torch.empty((plan.n, ld), dtype=self.dtype, device=self.device)[:, :m]
+                at = plan.gemm(at, out=out, out_dtype=self.dtype, bias=b, relu=True, stream=stream)
+            else:
+                at = plan.gemm(at, out_dtype=torch.float32, bias=b, relu=False, stream=stream)
+        return at
+
+    def logits(self, x) -> np.ndarray:
+        """x: M x K0 (host) -> M x N_last fp32 (host), like engine_logits."""
+        x = np.ascontiguousarray(np.asarray(x, np.float32))
+        xt = torch.from_numpy(x).to(self.device)
+        at = prep_activations(xt, Layout.ROW_MAJOR, self.dtype)
+        return self.forward_t(at).t().contiguous().cpu().numpy()
+
+
+def engine_logits(model, x, patterns, workers: int = 1, *, device=None, dtype=None) -> np.ndarray:
+    """trainer.py:232-250 drop-in: float32 forward pass through the TW-GEMM
+    with a bias+ReLU epilogue.  `model` is duck-typed (.weights, .biases, as
+    the reference's MlpModel); `workers` is accepted for signature parity."""
+    if len(patterns) != len(model.weights):
+        raise DimensionError("need one pattern per layer")
+    if workers < 1:
+        raise DimensionError(f"workers must be >= 1, got {workers}")
+    net = TwMlp(model.weights, model.biases, patterns, device=device, dtype=dtype)
+    return net.logits(x)

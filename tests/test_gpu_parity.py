@@ -292,3 +292,55 @@ def test_sharded_plan_single_rank_equals_full_plan():
     got = sp.gemm(at).cpu().numpy()
     full = tw.TwPlan(ts).gemm(at).cpu().numpy()
     assert np.array_equal(got, full)
+
+
+@pytest.mark.parametrize("relu,out_dtype", [(True, torch.float32), (False, torch.float32), (True, torch.float16)])
+def test_bias_relu_epilogue(relu, out_dtype):
+    """trainer.py:246-248 fused: relu?(C + bias) on every column; pruned
+    columns become the constant relu?(bias[j])."""
+    a, w, p = orc.bench_inputs(200, 256, 320, 64, 0.6, seed=31)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    bias = np.random.default_rng(5).standard_normal(320).astype(np.float32)
+    plan = tw.TwPlan(ts)
+    got = plan.gemm(device_at(a), out_dtype=out_dtype, bias=torch.from_numpy(bias).cuda(), relu=relu)
+    got = got.float().cpu().numpy()
+    c = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), 256, 320)) + bias[:, None]
+    want = np.maximum(c, 0) if relu else c
+    assert rel_l2(got, want) <= (1e-3 if out_dtype == torch.float32 else 2e-3)
+    pr = orc.pruned_columns(p)
+    const = np.maximum(bias[pr], 0) if relu else bias[pr]
+    assert np.array_equal(got[pr], np.repeat(const.astype(np.float32)[:, None], 200, axis=1).astype(
+        np.float16 if out_dtype == torch.float16 else np.float32).astype(np.float32))
+
+
+def test_engine_logits_layer_chain():
+    """trainer.py:232-250 engine_logits on the GPU: a 3-layer MLP through
+    three TW plans with the fused bias/ReLU epilogue and C^T -> A^T chaining.
+    Oracle: the reference's forward restated with numpy on the operands the
+    kernel sees (fp16-rounded weights and layer inputs)."""
+    rng = np.random.default_rng(11)
+    dims = [64, 96, 80, 10]
+    ws = [rng.standard_normal((dims[i], dims[i + 1])).astype(np.float32) * 0.3 for i in range(3)]
+    bs = [rng.standard_normal(dims[i + 1]).astype(np.float32) * 0.1 for i in range(3)]
+    ps = [orc.random_uniform_pattern(dims[i], dims[i + 1], 32, 0.5, seed=i) for i in range(3)]
+    x = rng.standard_normal((300, 64)).astype(np.float32)
+
+    class Model:
+        weights, biases = ws, bs
+
+    got = tw.engine_logits(Model, x, [to_tw_pattern(p) for p in ps])
+    assert got.shape == (300, 10) and got.dtype == np.float32
+    f16 = lambda v: v.astype(np.float16).astype(np.float64)  # noqa: E731
+    act = f16(x)
+    exact = x.astype(np.float64)
+    for i, (w, b, p) in enumerate(zip(ws, bs, ps)):
+        z = act @ f16(orc.zero_fill(w, p)) + b
+        ze = exact @ orc.zero_fill(w, p).astype(np.float64) + b
+        if i < 2:
+            act, exact = f16(np.maximum(z, 0)), np.maximum(ze, 0)
+        else:
+            act, exact = z, ze
+    assert rel_l2(got, act) <= 1e-3        # same rounded operands: accumulation order only
+    assert rel_l2(got, exact) <= 1e-2      # vs the all-fp32 reference forward (fp16 layer I/O)
+    with pytest.raises(tw.DimensionError):
+        tw.engine_logits(Model, x, [to_tw_pattern(p) for p in ps[:2]])
