@@ -4,6 +4,7 @@ one persistent sm_100a tcgen05 kernel, plus the TEW CSR SpMM and the
 N-sharded multi-GPU launcher.  See DESIGN.md."""
 
 from .matrix import (
+    ConfigError,
     CscMatrix,
     DenseMatrix,
     DimensionError,
@@ -36,7 +37,8 @@ from .pattern import (
 )
 from .sharded import ShardedTwPlan, all_gather_rows, shard_ranges
 from .layers import TwMlp, engine_logits
-from .formats import plan_from_files, read_csc, read_matrix, read_pattern, write_csc, write_matrix, write_pattern
+from .formats import (plan_from_files, read_csc, read_matrix, read_model, read_pattern, write_csc, write_matrix,
+                      write_pattern)
 from .engine import (
     DeviceCsc,
     FlopReport,

@@ -200,3 +200,54 @@ def plan_from_files(pattern_path, weights, device=None, dtype=None, col_range=No
         return PackedPlan._host_from_arrays(k, n, g, col_off, col_ids, words, subs, sub_off, col_range=col_range)
     return TwPlan._from_arrays(k, n, g, col_off, col_ids, words, subs, sub_off, device=device, dtype=dtype,
                                col_range=col_range)
+
+
+# ----------------------------------------------------------------- TWML
+_ML = struct.Struct("<II")  # version, layer count
+
+
+def _dense_record(raw: bytes, off: int):
+    if raw[off:off + 4] != b"TWMX":
+        raise FormatError(f"bad magic {raw[off:off + 4]!r}, expected {b'TWMX'!r}")
+    if len(raw) < off + 4 + _MX.size:
+        raise FormatError("header truncated")
+    version, rows, cols, layout = _MX.unpack_from(raw, off + 4)
+    if version != VERSION:
+        raise FormatError(f"unsupported version {version}")
+    if layout not in (0, 1) or rows == 0 or cols == 0:
+        raise FormatError(f"bad dense record ({rows}x{cols}, layout {layout})")
+    off += 4 + _MX.size
+    if len(raw) < off + 4 * rows * cols:
+        raise FormatError("dense record truncated")
+    m = DenseMatrix(rows, cols, Layout(layout), np.frombuffer(raw, "<f4", rows * cols, off).astype(np.float32))
+    return m, off + 4 * rows * cols
+
+
+def read_model(path):
+    """trainer.py:275-306 load_model (TWML checkpoint) -> (weights, biases):
+    lists of float32 arrays (K_i x N_i and N_i), for the verify CLI and the
+    layer-chaining caller.  (The trainer itself is out of scope.)"""
+    with open(path, "rb") as f:
+        raw = f.read()
+    _check_magic(raw, b"TWML")
+    (n_layers,) = _header(raw, _ML)
+    off = 4 + _ML.size
+    shapes = []
+    for _ in range(n_layers):
+        if len(raw) < off + 8:
+            raise FormatError("shape table truncated")
+        shapes.append(struct.unpack_from("<II", raw, off))
+        off += 8
+    weights, biases = [], []
+    for rows, cols in shapes:
+        w, off = _dense_record(raw, off)
+        if (w.rows, w.cols) != (rows, cols):
+            raise FormatError(f"layer blob ({w.rows},{w.cols}) does not match ({rows},{cols})")
+        b, off = _dense_record(raw, off)
+        if (b.rows, b.cols) != (1, cols):
+            raise FormatError(f"bias blob ({b.rows},{b.cols}) does not match (1,{cols})")
+        weights.append(w.array().astype(np.float32))
+        biases.append(b.array().astype(np.float32).ravel())
+    if off != len(raw):
+        raise FormatError(f"{len(raw) - off} trailing bytes in checkpoint")
+    return weights, biases

@@ -30,6 +30,10 @@ class FormatError(ValueError):
     """A binary file is malformed (matrix.py:38-39)."""
 
 
+class ConfigError(ValueError):
+    """A configuration value is out of range (pruning.py:24-25)."""
+
+
 @dataclass(frozen=True)
 class GemmShape:
     """matrix.py:42-54"""

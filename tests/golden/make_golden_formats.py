@@ -32,3 +32,11 @@ _, ew = ref.tew_overlay(wd, ref.magnitude_scores(wd), p, ref.TewConfig(alpha=sp 
 ref.write_csc(ew, os.path.join(OUT, "ew_g64.twcs"))
 for f in sorted(os.listdir(OUT)):
     print(f, os.path.getsize(os.path.join(OUT, f)))
+# a 2-layer TWML checkpoint + its pattern_<i>.twpt files (the `verify` CLI input)
+rng2 = np.random.default_rng(9)
+model = ref.MlpModel([rng2.standard_normal((64, 96)) * 0.2, rng2.standard_normal((96, 10)) * 0.2],
+                     [rng2.standard_normal(96) * 0.1, rng2.standard_normal(10) * 0.1])
+ref.save_model(model, os.path.join(OUT, "mlp.twml"))
+ref.write_pattern(ref.random_uniform_pattern(64, 96, 32, 0.5, seed=1), os.path.join(OUT, "pattern_0.twpt"))
+ref.write_pattern(ref.random_uniform_pattern(96, 10, 8, 0.5, seed=2), os.path.join(OUT, "pattern_1.twpt"))
+print("mlp.twml", os.path.getsize(os.path.join(OUT, "mlp.twml")))

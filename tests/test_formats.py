@@ -76,3 +76,26 @@ def test_plan_from_files_matches_compact_path():
 def test_plan_from_files_dimension_mismatch():
     with pytest.raises(tw.DimensionError):
         formats.plan_from_files(f("c2b.twpt"), f("w_g64.twmx"), host=True)
+
+
+def test_read_model_reference_checkpoint(tmp_path):
+    ws, bs = tw.read_model(f("mlp.twml"))
+    assert [w.shape for w in ws] == [(64, 96), (96, 10)] and [b.shape for b in bs] == [(96,), (10,)]
+    raw = open(f("mlp.twml"), "rb").read()
+    for i, bad in enumerate((raw[:30], raw + b"\0", b"XXXX" + raw[4:])):
+        p = tmp_path / f"bad{i}.twml"
+        p.write_bytes(bad)
+        with pytest.raises(tw.FormatError):
+            tw.read_model(p)
+
+
+def test_cli_exit_codes_without_gpu(tmp_path, capsys):
+    from paper_2008_13006_b200 import cli
+    # config error (repeats < 5, cli.py:383-384) -> 2
+    assert cli.main(["bench", "--repeats", "3", "--out", str(tmp_path / "b.csv")]) == cli.EXIT_CONFIG
+    # missing pattern files -> I/O error 3
+    assert cli.main(["verify", "--model", f("mlp.twml"), "--patterns", str(tmp_path)]) == cli.EXIT_IO
+    # malformed checkpoint -> format error 3
+    bad = tmp_path / "bad.twml"
+    bad.write_bytes(b"TWMLxx")
+    assert cli.main(["verify", "--model", str(bad), "--patterns", FMT]) == cli.EXIT_IO

@@ -10,7 +10,9 @@ and are checked bit-exactly.
 
 from __future__ import annotations
 
+import csv
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -344,3 +346,16 @@ def test_engine_logits_layer_chain():
     assert rel_l2(got, exact) <= 1e-2      # vs the all-fp32 reference forward (fp16 layer I/O)
     with pytest.raises(tw.DimensionError):
         tw.engine_logits(Model, x, [to_tw_pattern(p) for p in ps[:2]])
+
+
+def test_cli_verify_and_bench(tmp_path, capsys):
+    """The GPU verify / bench commands on reference-written files."""
+    from paper_2008_13006_b200 import cli
+    fmt = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fmt")
+    assert cli.main(["verify", "--model", os.path.join(fmt, "mlp.twml"), "--patterns", fmt, "--probes", "5"]) == 0
+    assert "PASS 5 probes x 2 layers" in capsys.readouterr().out
+    out = tmp_path / "b.csv"
+    assert cli.main(["bench", "--shapes", "256,768,3072", "--sparsities", "0,0.75", "--out", str(out)]) == 0
+    rows = list(csv.reader(open(out)))
+    assert rows[0][:17] == cli.BENCH_HEADER and len(rows) == 3
+    assert all(float(r[16]) <= 1e-4 * 768 for r in rows[1:])  # max_abs_diff within verify's tolerance
