@@ -266,6 +266,40 @@ __device__ __forceinline__ void store_rows(const GemmArgs &args, OutT *out, cons
   }
 }
 
+// Store phase for 16-bit staging: staged row r already holds the rounded
+// OutT values of tile column col_of(r) (RS tokens, row stride RS); each lane
+// moves 16 bytes (8 tokens) straight from shared to global memory.
+template <typename OutT, int kRows, int RS, typename ColOf>
+__device__ __forceinline__ void store_rows16(const GemmArgs &args, OutT *out, const float *buf_f, int r0, int lane,
+                                             int m0, ColOf col_of, const int32_t *ucol, int n_i, bool vec) {
+  if constexpr (sizeof(OutT) != 2) return;  // only instantiated for 16-bit outputs
+  const OutT *buf = reinterpret_cast<const OutT *>(buf_f);
+  constexpr int PER_ROW = RS / 8;  // 16-byte pieces per staged row (32 | 16)
+  uint4 vals[kRows];
+  int orows[kRows];
+  const bool on = lane < PER_ROW;
+#pragma unroll
+  for (int rb = 0; rb < kRows; ++rb) {
+    const int srow = r0 + rb;
+    const int col = col_of(srow);
+    orows[rb] = (col < n_i && !(args.debug & 2)) ? ucol[col] : -1;
+    vals[rb] = on ? *reinterpret_cast<const uint4 *>(buf + srow * RS + lane * 8) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int rb = 0; rb < kRows; ++rb) {
+    if (orows[rb] < 0 || !on) continue;
+    OutT *grow = out + (int64_t)orows[rb] * args.ldc + m0 + lane * 8;
+    if (vec && m0 + lane * 8 + 8 <= args.M) {
+      __stcs(reinterpret_cast<uint4 *>(grow), vals[rb]);
+    } else {
+      const uint16_t *h = reinterpret_cast<const uint16_t *>(&vals[rb]);
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+        if (m0 + lane * 8 + x < args.M) reinterpret_cast<uint16_t *>(grow)[x] = h[x];
+    }
+  }
+}
+
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
 // committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
@@ -564,6 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       epi_sync();  // sCol visible; previous unit's staging reads done
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 5);
       const bool mode_a = TB == 256 && nh == 2;
+      // 16-bit outputs without accumulate / bias are rounded while staging
+      const bool stage16 = sizeof(OutT) == 2 && !args.accumulate && args.bias == nullptr && !(args.debug & 1024);
       const bool mode_c = TB == 256 && nh == 1;
       const int ccols = mode_c ? 2 * CK : CK;  // tile columns per chunk
       const int n_chunks = (min(t.n_i, 128) + ccols - 1) / ccols;
@@ -582,10 +618,17 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         if (have) {
           ptx::tmem_ld_wait();
           if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 0);
-          float *dst = mode_a ? buf + h * 128 + q * 32 + lane : buf + h * CK * 128 + q * 32 + lane;
           const int rs = mode_a ? 256 : 128;
+          const int so = mode_a ? h * 128 + q * 32 + lane : h * CK * 128 + q * 32 + lane;
+          if (stage16) {  // 16-bit outputs: round once here, stage half the bytes
+            OutT *dst = reinterpret_cast<OutT *>(buf) + so;
 #pragma unroll
-          for (int jj = 0; jj < CK; ++jj) dst[jj * rs] = __uint_as_float(v[jj]);
+            for (int jj = 0; jj < CK; ++jj) dst[jj * rs] = cvt_out<OutT>(__uint_as_float(v[jj]));
+          } else {
+            float *dst = buf + so;
+#pragma unroll
+            for (int jj = 0; jj < CK; ++jj) dst[jj * rs] = __uint_as_float(v[jj]);
+          }
         }
         if (ci == n_chunks - 1) {
           // all of this warp's TMEM reads for the unit are done: hand the
@@ -604,7 +647,16 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         // 2) staged rows -> global.  All shared-memory reads of a batch are
         // issued before its first global store: an LDS queued behind a
         // backpressured STG in the same pipe would wait for it.
-        if (mode_a) {
+        if (stage16) {
+          if (mode_a)
+            store_rows16<OutT, 4, 256>(args, out, buf, e * 4, lane, m0, [&](int r) { return ci * CK + r; }, ucol,
+                                       t.n_i, vec);
+          else
+            store_rows16<OutT, 8, 128>(
+                args, out, buf, e * 8, lane, m0,
+                [&](int r) { return mode_c ? ci * ccols + r : (r < CK ? 0 : 128) + ci * CK + (r % CK); }, ucol,
+                t.n_i, vec);
+        } else if (mode_a) {
           store_rows<OutT, 4, 256>(args, out, buf, e * 4, lane, m0, 256, [&](int r) { return ci * CK + r; }, ucol,
                                    t.n_i, vec);
         } else {
