@@ -1,12 +1,15 @@
 """Benchmark: TW-sparse GEMM on B200 vs dense cuBLAS bf16 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--out-dtype fp32|fp16|bf16] [--workload C2a|C2b|C1|C5_75|C4]
+                    [--out-dtype fp16|fp32|bf16] [--workload C2a|C2b|C1|C5_75|C4]
 
 One step = one pass of the hot path over one batch: gemm_tw of the BERT-base
 FC1 layer (M=4096 tokens, K=768, N=3072, G=128, 75% TW sparsity, pattern
 random_uniform_pattern(seed 42), A/W ~ N(0,1) from default_rng(42) rounded
-to bf16 -- the reference's own bench recipe, cli.py:408-412).  Inputs are
+to bf16 -- the reference's own bench recipe, cli.py:408-412), fp32
+accumulation, fp16 output by default (same output bytes as the cuBLAS bf16
+baseline, rel-L2 ~2e-4 vs the fp32 oracle; --out-dtype fp32 for the
+reference's own output dtype -- both are reported).  Inputs are
 resident in HBM for `value` (A^T bf16, packed plan); `e2e` runs the
 reference-signature API with host fp32 buffers in pinned memory (H2D +
 transpose/cast + GEMM + D2H of the fp32 C inside the timed region).
@@ -320,14 +323,17 @@ def run_ours(args):
     plans = [plan] + [tw.TwPlan(ts, device=dev, col_range=col_range) for _ in range(n_sets - 1)]
     outs = [torch.empty((n_layer, m), dtype=out_dt, device=dev) for _ in range(n_sets)]
 
-    # parity gate (untimed): GPU result vs the CPU oracle on this rank's slice
-    ct = plan.gemm(at0, out_dtype=torch.float32).cpu().numpy()
+    # parity gate (untimed): GPU result (timed output dtype, and fp32) vs the
+    # CPU oracle on this rank's slice
     sub = orc.compact(w, p)
     want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(sub, k, n_total),
                           threads=orc.max_threads())[col_range[0]:col_range[1]]
+    prc = orc.pruned_columns(p)
+    prc = prc[(prc >= col_range[0]) & (prc < col_range[1])] - col_range[0]
+    ct = plan.gemm(at0, out_dtype=out_dt).float().cpu().numpy()
     parity = orc.rel_l2(ct, want)
-    zeros_ok = bool(np.all(ct[orc.pruned_columns(p)[(orc.pruned_columns(p) >= col_range[0]) &
-                                                   (orc.pruned_columns(p) < col_range[1])] - col_range[0]] == 0))
+    zeros_ok = bool(np.all(ct[prc] == 0))
+    parity_fp32 = orc.rel_l2(plan.gemm(at0, out_dtype=torch.float32).cpu().numpy(), want)
     del ct, want
 
     def step(i):
@@ -455,7 +461,8 @@ def run_ours(args):
             "speedup_vs_cublas_bf16_same_out_dtype": (result["cublas"]["fp32_out_ms"] if args.out_dtype == "fp32"
                                                       else result["cublas"]["bf16_out_ms"]) / ms,
             "cublas": result["cublas"], "variants": result["variants"],
-            "parity": {"rel_l2_vs_oracle": parity, "pruned_cols_exact_zero": zeros_ok, "bar": 1e-3},
+            "parity": {"rel_l2_vs_oracle": parity, "out_dtype": args.out_dtype, "rel_l2_fp32_out": parity_fp32,
+                       "pruned_cols_exact_zero": zeros_ok, "bar": 1e-3},
             "roofline": roofline, "cpu_baseline": result.get("cpu_baseline"), "e2e": result.get("e2e"),
             "gpu_launches": args.steps, "clocks": clk.summary(),
         }
@@ -475,7 +482,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2a", choices=sorted(WORKLOADS))
-    ap.add_argument("--out-dtype", default="fp32", choices=["fp32", "fp16", "bf16"])
+    # fp16 output: the same output bytes as cuBLAS bf16 (the metric's baseline)
+    # and within the 1e-3 parity bar (bf16 output is not: SURVEY finding 2)
+    ap.add_argument("--out-dtype", default="fp16", choices=["fp32", "fp16", "bf16"])
     ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds before timing (clock settle)")
     ap.add_argument("--cpu-sample-m", type=int, default=4096)
     ap.add_argument("--no-cpu", action="store_true")
