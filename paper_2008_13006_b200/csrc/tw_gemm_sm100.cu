@@ -589,7 +589,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       // suspend the warp for up to its time limit between zero rows)
       const bool fill = args.zero_policy == 0 || (args.zero_policy == 1 && j == u_end - 1);
       while (e == 0 && fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
-        if (lane == 0 && bulk_ok) ptx::bulk_wait_read<2>();
+        if (lane == 0 && bulk_ok) {
+          if (args.debug & 2048) ptx::bulk_wait_read<2>(); else ptx::bulk_wait_read<0>();
+        }
         zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
         ++zr;
       }
