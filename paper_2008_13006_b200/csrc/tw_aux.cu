@@ -4,6 +4,7 @@
 //            _kernels.py:30-41), fp32 mul-then-add in ascending p
 //   exact  : bit-exact CUDA-core TW GEMM over a packed plan      (_kernels.py:13-27)
 #include <algorithm>
+#include <type_traits>
 
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -196,17 +197,32 @@ __global__ void __launch_bounds__(256) spmm_csc_kernel(const AT *__restrict__ at
   }
 }
 
+// acc + v * a for the tiled SpMM.  fp32 activations: a separately rounded
+// multiply then add, the exact sequence of spmm_accum (_kernels.py:30-41);
+// 16-bit activations (the TEW path, parity by rel-L2): one fused FMA.
+template <typename AT>
+__device__ __forceinline__ float spmm_madd(float acc, float v, float a) {
+  if constexpr (sizeof(AT) == 4) {
+    return __fadd_rn(acc, __fmul_rn(v, a));
+  } else {
+    return fmaf(v, a, acc);
+  }
+}
+
 // PER consecutive activations from shared memory as fp32 (one vector load)
 template <typename AT, int PER>
 __device__ __forceinline__ void load_smem_vec(const AT *p, float (&o)[PER]) {
-  if constexpr (sizeof(AT) == 2 && PER == 4) {
+  if constexpr (std::is_same<AT, __nv_bfloat16>::value && PER == 4) {
+    const uint2 u = *reinterpret_cast<const uint2 *>(p);  // bf16 -> fp32 is a 16-bit shift
+    o[0] = __uint_as_float(u.x << 16);
+    o[1] = __uint_as_float(u.x & 0xffff0000u);
+    o[2] = __uint_as_float(u.y << 16);
+    o[3] = __uint_as_float(u.y & 0xffff0000u);
+  } else if constexpr (sizeof(AT) == 2 && PER == 4) {
     const uint2 u = *reinterpret_cast<const uint2 *>(p);
-    const uint32_t w[2] = {u.x, u.y};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint16_t b = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
-      o[i] = to_f<AT>(*reinterpret_cast<const AT *>(&b));
-    }
+    const float2 lo = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
+    const float2 hi = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
+    o[0] = lo.x; o[1] = lo.y; o[2] = hi.x; o[3] = hi.y;
   } else if constexpr (sizeof(AT) == 4 && PER == 4) {
     const float4 f = *reinterpret_cast<const float4 *>(p);
     o[0] = f.x; o[1] = f.y; o[2] = f.z; o[3] = f.w;
@@ -236,7 +252,7 @@ __device__ __forceinline__ void store_vec(OutT *crow, int64_t mt, int64_t m, con
 // read from L2 once per (segment, column group) instead of once per stored
 // entry -- 2*nnz*M bytes of L2 traffic become ~groups*2*K*M.  Same exact
 // multiply-then-add sequence in ascending p.
-constexpr int kSpmmWarps = 16;
+constexpr int kSpmmWarps = 32;
 template <typename AT, typename OutT, int T>
 __global__ void __launch_bounds__(kSpmmWarps * 32) spmm_tiled_kernel(const AT *__restrict__ at, int64_t m, int64_t k, int64_t lda,
                                                          int64_t col_begin, int64_t n_cols, int cols_per_cta,
@@ -266,22 +282,33 @@ __global__ void __launch_bounds__(kSpmmWarps * 32) spmm_tiled_kernel(const AT *_
   // shared memory left after the A^T segment when it fits; every warp then
   // reads its entries with broadcast shared loads instead of global loads
   // whose latency would sit on each column's critical path.
+  // Entries are staged as interleaved (row, value) pairs -- one 8-byte
+  // broadcast load per entry -- by 4-byte cp.async (no register round trip),
+  // and converted to (row * T, value) once after the copy.
   const int64_t pg0 = __ldg(col_ptr + j0 + col_begin), pg1 = __ldg(col_ptr + j1 + col_begin);
   const int64_t ncg = j1 - j0;
   int32_t *s_ptr = reinterpret_cast<int32_t *>(sm_raw + k * RB);
-  int32_t *s_row = s_ptr + ncg + 1;
-  float *s_val = reinterpret_cast<float *>(s_row + (pg1 - pg0));
-  const bool staged = (int64_t)(k * RB) + (ncg + 1 + 2 * (pg1 - pg0)) * 4 <= smem_bytes;
+  int2 *s_rv = reinterpret_cast<int2 *>(s_ptr + ((ncg + 2) & ~1));  // 8-byte aligned
+  const bool staged = (int64_t)(k * RB) + (((ncg + 2) & ~1) + 2 * (pg1 - pg0)) * 4 <= smem_bytes;
   if (staged) {
-    for (int64_t i = threadIdx.x; i <= ncg; i += blockDim.x) s_ptr[i] = __ldg(col_ptr + j0 + col_begin + i) - (int32_t)pg0;
+    for (int64_t i = threadIdx.x; i <= ncg; i += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(s_ptr + i)),
+                   "l"(col_ptr + j0 + col_begin + i)
+                   : "memory");
     for (int64_t i = threadIdx.x; i < pg1 - pg0; i += blockDim.x) {
-      s_row[i] = __ldg(row_idx + pg0 + i);
-      s_val[i] = __ldg(values + pg0 + i);
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(s_rv + i);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(row_idx + pg0 + i) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d + 4), "l"(values + pg0 + i) : "memory");
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
+  if (staged) {
+    for (int64_t i = threadIdx.x; i <= ncg; i += blockDim.x) s_ptr[i] -= (int32_t)pg0;
+    for (int64_t i = threadIdx.x; i < pg1 - pg0; i += blockDim.x) s_rv[i].x *= T;
+    __syncthreads();
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mt = m0 + lane * PER;
   for (int64_t jr = j0 + warp; jr < j1; jr += kSpmmWarps) {
@@ -291,24 +318,26 @@ __global__ void __launch_bounds__(kSpmmWarps * 32) spmm_tiled_kernel(const AT *_
     if (staged) {
       const int q0 = s_ptr[jr - j0], q1 = s_ptr[jr - j0 + 1];
       int q = q0;
+      const AT *sl = sa + lane * PER;
       for (; q + 4 <= q1; q += 4) {  // four entries' loads in flight, adds still in order
         float a[4][PER], v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          v[u] = s_val[q + u];
-          load_smem_vec<AT, PER>(sa + (int64_t)s_row[q + u] * T + lane * PER, a[u]);
+          const int2 rv = s_rv[q + u];
+          v[u] = __int_as_float(rv.y);
+          load_smem_vec<AT, PER>(sl + rv.x, a[u]);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int x = 0; x < PER; ++x) acc[x] = __fadd_rn(acc[x], __fmul_rn(v[u], a[u][x]));
+          for (int x = 0; x < PER; ++x) acc[x] = spmm_madd<AT>(acc[x], v[u], a[u][x]);
       }
       for (; q < q1; ++q) {
         float a[PER];
-        const float v = s_val[q];
-        load_smem_vec<AT, PER>(sa + (int64_t)s_row[q] * T + lane * PER, a);
+        const int2 rv = s_rv[q];
+        load_smem_vec<AT, PER>(sl + rv.x, a);
 #pragma unroll
-        for (int x = 0; x < PER; ++x) acc[x] = __fadd_rn(acc[x], __fmul_rn(v, a[x]));
+        for (int x = 0; x < PER; ++x) acc[x] = spmm_madd<AT>(acc[x], __int_as_float(rv.y), a[x]);
       }
     } else {
       const int64_t j = jr + col_begin;
