@@ -292,13 +292,26 @@ def run_ours(args):
     from oracle import oracle as orc  # checker + cpu_baseline only
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # TW_B200_BENCH_BACKEND=gloo exercises the N > 1 path on a box with fewer
+    # GPUs than ranks (ranks share devices; timings are then meaningless):
+    # the driver's multi-GPU runs use NCCL, one rank per GPU.
+    backend = os.environ.get("TW_B200_BENCH_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist
+
+    def allreduce_max(x: float) -> float:
+        t = torch.tensor([x], device=dev if backend == "nccl" else "cpu")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
     m, k, n_layer, g, s, desc = WORKLOADS[args.workload]
     hbm_peak, tc_peak, peak_kind = load_peaks()
     out_dt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[args.out_dtype]
@@ -352,9 +365,7 @@ def run_ours(args):
     barrier()
     ms_all = ms
     if pg is not None:
-        t = torch.tensor([ms], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms_all = float(t.item())
+        ms_all = allreduce_max(ms)
     value = world * dense_flops / (ms_all * 1e-3) / 1e12
 
     # ---- dominant kernel roofline: the TW kernel is the only launch per step
@@ -435,14 +446,13 @@ def run_ours(args):
 
     # ---- multi-GPU: NCCL all-gather that reassembles C^T (not in `value`)
     if pg is not None:
-        full = torch.empty((n_total, m), dtype=out_dt, device=dev)
+        full = torch.empty((n_total, m), dtype=out_dt, device=dev if backend == "nccl" else "cpu")
         def ag(i):
-            pg.all_gather_into_tensor(full, outs[i % n_sets])
+            src = outs[i % n_sets] if backend == "nccl" else outs[i % n_sets].cpu()
+            pg.all_gather_into_tensor(full, src)
         barrier()
         ag_ms = time_device(torch, ag, max(3, args.steps // 4), 2, graph=False)
-        t = torch.tensor([ag_ms], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        result["allgather"] = {"ms": float(t.item()), "bytes_per_rank_in": (world - 1) * out_bytes * n_layer * m,
+        result["allgather"] = {"ms": allreduce_max(ag_ms), "backend": backend, "bytes_per_rank_in": (world - 1) * out_bytes * n_layer * m,
                                "note": "ncclAllGather of C^T row blocks over NVLink; reported, not in value"}
 
     if rank == 0:

@@ -70,6 +70,11 @@ def all_gather_rows(local, n: int, group=None, out=None):
     if world == 1:
         if out.data_ptr() != local.data_ptr():
             out.copy_(local)
+    elif local.is_cuda and dist.get_backend(group) != "nccl":
+        # gloo (host-logic tests, several ranks per device): stage via the host
+        host = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(host, local.contiguous().cpu(), group=group)
+        out.copy_(host)
     else:
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
     return out[:n]
