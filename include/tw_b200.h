@@ -206,6 +206,12 @@ int tw_gemm_tew(const tw_plan *plan, const void *at, int64_t m, int64_t lda, con
 int tw_gemm_traced(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
                    int out_dtype, int64_t *trace, void *stream);
 
+/* Strided (2-D) async copy for the reference-signature API's pipelined
+ * host round trip (token chunks of A in, token columns of C^T out):
+ * kind 0 host->device, 1 device->host, 2 device->device. */
+int tw_copy_2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width_bytes, int64_t height,
+               int kind, void *stream);
+
 /* Number of SMs used by the persistent grid on the current device. */
 int tw_device_sm_count(int *sms);
 

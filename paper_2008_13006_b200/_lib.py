@@ -58,6 +58,7 @@ SIGNATURES = {
     "tw_spmm_csc": (_i32, [_p, _i32, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _i32, _i32, _p]),
     "tw_gemm_tew": (_i32, [_p, _p, _i64, _i64, _p, _p, _p, _i64, _p, _i64, _i32, _p]),
     "tw_device_sm_count": (_i32, [ctypes.POINTER(ctypes.c_int)]),
+    "tw_copy_2d": (_i32, [_p, _i64, _p, _i64, _i64, _i64, _i32, _p]),
 }
 
 _lock = threading.Lock()

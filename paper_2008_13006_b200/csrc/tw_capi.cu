@@ -122,6 +122,19 @@ using namespace tw;
 
 extern "C" {
 
+int tw_copy_2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width_bytes, int64_t height,
+               int kind, void *stream) {
+  clear_error();
+  if (width_bytes < 0 || height < 0 || dpitch < width_bytes || spitch < width_bytes)
+    return fail(TW_ERR_DIMENSION, "bad 2-D copy extents");
+  if (width_bytes == 0 || height == 0) return TW_OK;
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+  cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width_bytes, (size_t)height, k,
+                                    reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync");
+  return TW_OK;
+}
+
 int tw_device_sm_count(int *sms) {
   int major = 0;
   return sm_count_of_current(sms, &major);

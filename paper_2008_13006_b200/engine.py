@@ -20,6 +20,7 @@ compute call raises.  `workers` is accepted for signature compatibility
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass
 
@@ -387,9 +388,62 @@ def gemm_tw(a: DenseMatrix, tiles: CompactTileSet, workers: int = 1, *, device=N
     if a.rows == 0:
         return DenseMatrix(0, tiles.n, Layout.COL_MAJOR, np.zeros(0, np.float32))
     plan = _plan_for(tiles, device)
+    if a.layout == Layout.ROW_MAJOR and a.rows >= 2 * _PIPE_CHUNK and _PIPE_ON:
+        return _gemm_tw_pipelined(a, plan, device, out)
     at = _device_activations(a, device, plan.dtype)
     ct = plan.gemm(at, out_dtype=torch.float32)
     return _to_host_colmajor(ct, a.rows, tiles.n, out)
+
+
+_PIPE_CHUNK = int(os.environ.get("TW_B200_PIPE_CHUNK", "1024"))
+_PIPE_ON = os.environ.get("TW_B200_PIPE", "1") != "0"
+_pipe_streams: dict = {}
+
+
+def _gemm_tw_pipelined(a: DenseMatrix, plan: "TwPlan", device, out=None) -> DenseMatrix:
+    """gemm_tw's host round trip in token chunks on three streams: the H2D
+    copy + transpose/cast of chunk c+1, the TW-GEMM of chunk c and the 2-D
+    D2H copy of C^T's columns for chunk c-1 overlap (PCIe is full duplex).
+    Every chunk is the same kernel on a token slice (A^T columns / C^T
+    columns with the full row pitch), so the result is identical to the
+    one-shot path."""
+    m, k, n = a.rows, a.cols, plan.n
+    key = str(device)
+    if key not in _pipe_streams:
+        _pipe_streams[key] = (torch.cuda.Stream(device), torch.cuda.Stream(device))
+    s_in, s_out = _pipe_streams[key]
+    cur = torch.cuda.current_stream(device)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # frozen (read-only) buffers are only read here
+        a_host = torch.from_numpy(np.asarray(a.data, np.float32)).view(m, k)
+    if out is None:
+        buf = np.empty(m * n, np.float32)
+    else:
+        buf = np.asarray(out).reshape(-1)
+        if buf.dtype != np.float32 or buf.size != m * n:
+            raise DimensionError(f"out must hold {m * n} float32 values")
+    a_dev = torch.empty((m, k), dtype=torch.float32, device=device)
+    ld = (m + 7) // 8 * 8
+    at = torch.empty((k, ld), dtype=plan.dtype, device=device)[:, :m]
+    ct = torch.empty((n, m), dtype=torch.float32, device=device)
+    s_in.wait_stream(cur)
+    s_out.wait_stream(cur)
+    pinned = a_host.is_pinned()
+    for c0 in range(0, m, _PIPE_CHUNK):
+        c1 = min(m, c0 + _PIPE_CHUNK)
+        with torch.cuda.stream(s_in):
+            a_dev[c0:c1].copy_(a_host[c0:c1], non_blocking=pinned)
+            prep_activations(a_dev[c0:c1], Layout.ROW_MAJOR, plan.dtype, out=at[:, c0:c1], stream=s_in)
+        cur.wait_stream(s_in)
+        plan.gemm(at[:, c0:c1], out=ct[:, c0:c1], out_dtype=torch.float32, stream=cur)
+        s_out.wait_stream(cur)
+        _lib.call("tw_copy_2d", buf.ctypes.data + c0 * 4, m * 4, ct.data_ptr() + c0 * 4, m * 4, (c1 - c0) * 4, n, 1,
+                  s_out.cuda_stream)
+    s_out.synchronize()
+    cur.wait_stream(s_out)
+    a_dev.record_stream(s_in)
+    return DenseMatrix(m, n, Layout.COL_MAJOR, buf)
 
 
 def _device_csc(s: CscMatrix, device) -> DeviceCsc:

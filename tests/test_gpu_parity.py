@@ -359,3 +359,19 @@ def test_cli_verify_and_bench(tmp_path, capsys):
     rows = list(csv.reader(open(out)))
     assert rows[0][:17] == cli.BENCH_HEADER and len(rows) == 3
     assert all(float(r[16]) <= 1e-4 * 768 for r in rows[1:])  # max_abs_diff within verify's tolerance
+
+
+def test_reference_api_pipelined_round_trip_matches_device_path():
+    """gemm_tw on a large host A takes the chunked 3-stream path (H2D /
+    kernel / 2-D D2H overlapped); it must equal the device-resident result
+    bit for bit (same kernel per token slice), pinned or pageable buffers."""
+    a, w, p = orc.bench_inputs(4096 + 256, 768, 1000, 128, 0.75, seed=41)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    want = tw.TwPlan(ts).gemm(device_at(a)).cpu().numpy()
+    got = tw.gemm_tw(tw.DenseMatrix.from_array(a), ts)
+    assert got.layout == tw.Layout.COL_MAJOR and np.array_equal(got.data.reshape(1000, -1), want)
+    a_pin = torch.empty(a.size, dtype=torch.float32).pin_memory()
+    a_pin.copy_(torch.from_numpy(a.reshape(-1)))
+    out = torch.empty(want.size, dtype=torch.float32).pin_memory().numpy()
+    got2 = tw.gemm_tw(tw.DenseMatrix(a.shape[0], a.shape[1], tw.Layout.ROW_MAJOR, a_pin.numpy()), ts, out=out)
+    assert np.array_equal(got2.data.reshape(1000, -1), want)
