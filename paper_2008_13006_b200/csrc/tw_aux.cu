@@ -445,8 +445,11 @@ cudaError_t spmm_tiled(const void *at, int64_t m, int64_t k, int64_t lda, int64_
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   // enough CTAs for ~2 waves, as few column groups (A^T re-reads) as that allows
+  // one CTA per SM (the A^T segment fills shared memory): as many column
+  // groups as make whole waves -- floor(2 * SMs / segments) -- so the last
+  // wave is not a sliver (each group re-reads the segment from L2)
   const int64_t groups =
-      std::max<int64_t>(1, std::min<int64_t>((n_cols + kSpmmWarps - 1) / kSpmmWarps, (2 * sms + segs - 1) / segs));
+      std::max<int64_t>(1, std::min<int64_t>((n_cols + kSpmmWarps - 1) / kSpmmWarps, (2 * sms) / segs));
   const int cpc = (int)((n_cols + groups - 1) / groups);
   dim3 grid((unsigned)segs, (unsigned)((n_cols + cpc - 1) / cpc));
   kern<<<grid, kSpmmWarps * 32, smem, s>>>(reinterpret_cast<const AT *>(at), m, k, lda, col_begin, n_cols, cpc, cp, ri, va,
