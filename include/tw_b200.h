@@ -168,6 +168,18 @@ int tw_gemm(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *c
 int tw_gemm_bias(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
                  int out_dtype, const float *bias, int relu, void *stream);
 
+/* General form of tw_gemm / tw_gemm_bias.  flags: TW_GEMM_ACCUMULATE (add
+ * into ct, pruned rows untouched -- gemm_tew's second pass) and/or
+ * TW_GEMM_KEEP_PRUNED (write only the kept columns' rows and leave the
+ * pruned-column rows of ct as they are: for a resident output buffer whose
+ * pruned rows already hold their value -- 0, or relu?(bias) with the bias
+ * epilogue -- from an earlier full call, e.g. layer-chain activations).
+ * bias may be NULL. */
+#define TW_GEMM_ACCUMULATE 1
+#define TW_GEMM_KEEP_PRUNED 2
+int tw_gemm_ex(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
+               int flags, const float *bias, int relu, void *stream);
+
 /* Bit-exact CUDA-core variant of tw_gemm: fp32 multiply then fp32 add, in
  * ascending k per element (exactly mm_accum's rounding sequence); used to
  * prove layouts/indexing independent of tensor-core accumulation order.

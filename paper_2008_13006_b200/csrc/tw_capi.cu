@@ -207,9 +207,16 @@ int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, 
 int tw_gemm_bias(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
                  const float *bias, int relu, void *stream) {
   if (!bias) return fail(TW_ERR_ARG, "null bias");
+  return tw_gemm_ex(p, at, m, lda, ct, ldc, out_dtype, 0, bias, relu, stream);
+}
+
+int tw_gemm_ex(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
+               int flags, const float *bias, int relu, void *stream) {
   if (!p) return fail(TW_ERR_ARG, "null plan");
+  if ((flags & TW_GEMM_ACCUMULATE) && bias) return fail(TW_ERR_ARG, "bias epilogue cannot accumulate");
   // bias is indexed by global output column; the kernel indexes by plan row
-  return gemm_impl(p, at, m, lda, ct, ldc, out_dtype, 0, nullptr, stream, bias + p->host.col_begin, relu ? 1 : 0);
+  return gemm_impl(p, at, m, lda, ct, ldc, out_dtype, flags, nullptr, stream, bias ? bias + p->host.col_begin : nullptr,
+                   relu ? 1 : 0);
 }
 
 int tw_gemm_traced(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
@@ -243,7 +250,9 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
       return fail(TW_ERR_ARG, "activations need lda % 8 == 0 and a 16-byte aligned base (16-byte row gathers)");
   }
   const tw_dev_schedule *sched = nullptr;
-  if ((rc = get_schedule(p, m, out_size(out_dtype), !accumulate, sms, &sched))) return rc;
+  const bool accum = (accumulate & TW_GEMM_ACCUMULATE) != 0;
+  const bool keep_pruned = (accumulate & TW_GEMM_KEEP_PRUNED) != 0;
+  if ((rc = get_schedule(p, m, out_size(out_dtype), !accum && !keep_pruned, sms, &sched))) return rc;
   GemmArgs a{};
   a.tiles = p->d_tiles;
   a.kidx = p->d_kidx;
@@ -260,7 +269,8 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.at = at;
   a.lda = lda;
   a.M = (int32_t)m;
-  a.accumulate = accumulate ? 1 : 0;
+  a.accumulate = accum ? 1 : 0;
+  a.keep_pruned = keep_pruned ? 1 : 0;
   a.wbytes = hp.wrows * 128;
   // kind::f16 instruction descriptor: D f32 [4,6)=1, A/B bf16 [7,10)/[10,13)=1
   // (fp16 = 0), A MN-major [15]=1, B K-major [16]=0, M=128 -> [24,29)=8.

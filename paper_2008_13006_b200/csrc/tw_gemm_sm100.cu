@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     volatile int32_t *s_zdone = reinterpret_cast<volatile int32_t *>(tmem_holder + 1);
     // the output may be read / written by the previous kernel (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int z1 = (args.accumulate || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
+    const int z1 = (args.accumulate || args.keep_pruned || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
     constexpr int CK = C::kChunk;              // 32 accumulator columns per TMEM load
     int acc = 0;
     uint32_t acc_phase = 0;

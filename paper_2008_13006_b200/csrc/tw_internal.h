@@ -99,6 +99,7 @@ struct GemmArgs {
   int64_t *trace;     // optional per-CTA event timeline (tw_gemm_traced), else null
   const float *bias;  // optional per-output-row bias (fp32, row-rebased), fused epilogue
   int32_t relu;       // 1: max(x, 0) after the bias (trainer.py:246-248)
+  int32_t keep_pruned;  // 1: pruned-column rows are left untouched (resident output)
   int32_t zero_policy; // when the epilogue writes zero rows (kernel comment); env TW_B200_ZERO
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };

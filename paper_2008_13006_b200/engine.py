@@ -212,32 +212,37 @@ class TwPlan(PackedPlan):
             raise DimensionError(f"out must be a ({self.n_rows}, {m}) row-contiguous {out_dtype} tensor")
         return out
 
-    def gemm(self, at, out=None, out_dtype=None, accumulate=False, stream=None, bias=None, relu=False):
+    def gemm(self, at, out=None, out_dtype=None, accumulate=False, stream=None, bias=None, relu=False,
+             write_pruned=True):
         """C^T (N x M) = (A * expand(tiles))^T for A^T (K x M) -- engine.py:152-164.
         Pruned columns are exact zeros unless accumulate=True (then they are
         left untouched and kept columns are added into `out`).
 
         bias (fp32 CUDA tensor of length N) / relu: the trainer's epilogue
         (trainer.py:246-248) fused into the kernel -- relu?(C + bias) for
-        every output column, pruned ones included."""
+        every output column, pruned ones included.
+
+        write_pruned=False (needs `out`): leave the pruned-column rows of `out`
+        untouched -- for a resident output buffer whose pruned rows already
+        hold their value (0, or relu?(bias)) from an earlier full call."""
         out_dtype = out_dtype or torch.float32
         m, lda = self._check_at(at)
-        if accumulate and out is None:
-            raise ValueError("accumulate=True needs out")
+        if (accumulate or not write_pruned) and out is None:
+            raise ValueError("accumulate=True / write_pruned=False need out")
         ct = self._out(m, out, out_dtype)
+        flags = (1 if accumulate else 0) | (0 if write_pruned else 2)
+        bias_ptr = None
         if bias is not None:
             if accumulate:
                 raise ValueError("bias epilogue cannot be combined with accumulate")
             if not (isinstance(bias, torch.Tensor) and bias.is_cuda and bias.dtype == torch.float32
                     and bias.numel() == self.n and bias.is_contiguous()):
                 raise DimensionError(f"bias must be a contiguous fp32 CUDA tensor of {self.n} elements")
-            _lib.call("tw_gemm_bias", self._h, at.data_ptr(), m, lda, ct.data_ptr(), ct.stride(0), _code(out_dtype),
-                      bias.data_ptr(), 1 if relu else 0, _stream_ptr(stream))
-            return ct
-        if relu:
+            bias_ptr = bias.data_ptr()
+        elif relu:
             raise ValueError("relu needs the bias epilogue (pass bias=zeros for a plain ReLU)")
-        _lib.call("tw_gemm", self._h, at.data_ptr(), m, lda, ct.data_ptr(), ct.stride(0), _code(out_dtype),
-                  1 if accumulate else 0, _stream_ptr(stream))
+        _lib.call("tw_gemm_ex", self._h, at.data_ptr(), m, lda, ct.data_ptr(), ct.stride(0), _code(out_dtype),
+                  flags, bias_ptr, 1 if relu else 0, _stream_ptr(stream))
         return ct
 
     def gemm_exact(self, at32, out=None, stream=None):

@@ -36,6 +36,7 @@ class TwMlp:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dtype = dtype or torch.float16
         self.plans, self.biases = [], []
+        self._acts = {}
         for w, b, p in zip(weights, biases, patterns):
             ts = compact(DenseMatrix.from_array(np.asarray(w, np.float32)), p)
             self.plans.append(TwPlan(ts, device=self.device, dtype=self.dtype))
@@ -47,15 +48,27 @@ class TwMlp:
             if a.n != b.k:
                 raise DimensionError(f"layer output {a.n} does not match next layer input {b.k}")
 
+    def _act(self, i, m):
+        """Resident activation buffer of layer i for M tokens.  Its pruned
+        rows hold the constant relu(bias[j]) after the first call, so later
+        calls skip them (write_pruned=False): the kernel writes only the kept
+        columns' rows."""
+        key = (i, m)
+        if key not in self._acts:
+            ld = (m + 7) // 8 * 8  # next layer gathers 16-byte row chunks
+            self._acts[key] = [torch.empty((self.plans[i].n, ld), dtype=self.dtype, device=self.device)[:, :m], False]
+        return self._acts[key]
+
     def forward_t(self, at, stream=None):
         """A^T (K0 x M, plan dtype) -> logits^T (N_last x M, fp32), all on device."""
         last = len(self.plans) - 1
         for i, (plan, b) in enumerate(zip(self.plans, self.biases)):
             m = at.shape[1]
             if i < last:
-                ld = (m + 7) // 8 * 8  # next layer gathers 16-byte row chunks
-                out = torch.empty((plan.n, ld), dtype=self.dtype, device=self.device)[:, :m]
-                at = plan.gemm(at, out=out, out_dtype=self.dtype, bias=b, relu=True, stream=stream)
+                slot = self._act(i, m)
+                at = plan.gemm(at, out=slot[0], out_dtype=self.dtype, bias=b, relu=True, stream=stream,
+                               write_pruned=not slot[1])
+                slot[1] = True
             else:
                 at = plan.gemm(at, out_dtype=torch.float32, bias=b, relu=False, stream=stream)
         return at

@@ -375,3 +375,28 @@ def test_reference_api_pipelined_round_trip_matches_device_path():
     out = torch.empty(want.size, dtype=torch.float32).pin_memory().numpy()
     got2 = tw.gemm_tw(tw.DenseMatrix(a.shape[0], a.shape[1], tw.Layout.ROW_MAJOR, a_pin.numpy()), ts, out=out)
     assert np.array_equal(got2.data.reshape(1000, -1), want)
+
+
+def test_keep_pruned_rows_resident_output():
+    """write_pruned=False writes only the kept columns' rows: pruned rows of a
+    resident buffer keep their earlier value; the kept rows equal a full call."""
+    a, w, p = orc.bench_inputs(512, 384, 640, 128, 0.75, seed=51)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    plan = tw.TwPlan(ts)
+    at = device_at(a)
+    full = plan.gemm(at, out_dtype=torch.float16)
+    out = torch.full_like(full, 7.0)
+    plan.gemm(at, out=out, out_dtype=torch.float16, write_pruned=False)
+    pr = orc.pruned_columns(p)
+    kept = np.setdiff1d(np.arange(640), pr)
+    o, f = out.float().cpu().numpy(), full.float().cpu().numpy()
+    assert np.all(o[pr] == 7.0) and np.array_equal(o[kept], f[kept])
+    with pytest.raises(ValueError):
+        plan.gemm(at, write_pruned=False)
+    # layer chain: the second forward reuses resident activations
+    w2 = orc.bench_inputs(8, 640, 384, 128, 0.0, seed=4)[1]
+    net = tw.TwMlp([w, w2], [np.full(640, -0.5, np.float32), np.ones(384, np.float32)],
+                   [to_tw_pattern(p), to_tw_pattern(orc.random_uniform_pattern(640, 384, 128, 0.5, 2))])
+    x = orc.bench_inputs(96, 384, 8, 8, 0.0, seed=3)[0]
+    r1, r2 = net.logits(x), net.logits(x)
+    assert np.array_equal(r1, r2)
