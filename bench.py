@@ -470,6 +470,43 @@ def run_ours(args):
         ag_ms = time_device(torch, ag, max(3, args.steps // 4), 2, graph=False)
         result["allgather"] = {"ms": allreduce_max(ag_ms), "backend": backend, "bytes_per_rank_in": (world - 1) * out_bytes * n_layer * m,
                                "note": "ncclAllGather of C^T row blocks over NVLink; reported, not in value"}
+        # full layer on every rank: ShardedTwPlan.gemm = per-round TW-GEMM +
+        # in-place all-gather, round j's gather overlapping round j+1's GEMM
+        pipe = {}
+        for rounds in (1, 4):
+            sp = tw.ShardedTwPlan(ts, group=None, device=dev, rounds=rounds)
+            barrier()
+            pms = time_device(torch, lambda i: sp.gemm(ats[i % n_sets], out_dtype=out_dt),
+                              max(3, args.steps // 4), max(3, n_sets), graph=False)
+            pipe[f"rounds{rounds}_ms"] = allreduce_max(pms)
+            del sp
+        result["allgather"]["sharded_gemm_full_output"] = pipe
+        # e2e at N GPUs: host fp32 A (pinned) -> H2D + A^T prep -> sharded
+        # gemm (fp32, rounds 4) -> D2H of the full C^T on every rank
+        sp = tw.ShardedTwPlan(ts, group=None, device=dev, rounds=4)
+        a_pin = torch.empty((m, k), dtype=torch.float32, pin_memory=True)
+        a_pin.copy_(torch.from_numpy(a))
+        c_pin = torch.empty((n_total, m), dtype=torch.float32, pin_memory=True)
+        a_dev = torch.empty((m, k), dtype=torch.float32, device=dev)
+
+        def e2e_step():
+            a_dev.copy_(a_pin, non_blocking=True)
+            ct = sp.gemm(tw.prep_activations(a_dev), out_dtype=torch.float32)
+            c_pin.copy_(ct, non_blocking=True)
+            torch.cuda.synchronize()
+        for _ in range(3):
+            e2e_step()
+        barrier()
+        e_steps = max(3, min(args.steps, 30))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        e2e_s = allreduce_max((time.perf_counter() - t0) / e_steps)
+        result["e2e"] = {"value": world * dense_flops / e2e_s / 1e12, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
+                         "h2d_bytes_per_step": 4 * m * k, "d2h_bytes_per_step": 4 * m * n_total,
+                         "api": "ShardedTwPlan(rounds=4).gemm on prep_activations(H2D of pinned fp32 A); "
+                                "D2H of the gathered fp32 C^T (per rank)"}
+        del sp
 
     if rank == 0:
         line = {

@@ -19,6 +19,8 @@ NVLink/NVSwitch on a B200 box, gloo for the CPU tests of the host logic).
 
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 
 try:
@@ -80,52 +82,116 @@ def all_gather_rows(local, n: int, group=None, out=None):
     return out[:n]
 
 
+def cyclic_ranges(n: int, world: int, rounds: int) -> list[list[tuple[int, int]]]:
+    """Block-cyclic output-column chunks: chunk c = j*world + r covers
+    [c*s, (c+1)*s) (clipped to N), s = ceil(N / (world*rounds)); rank r owns
+    chunks r, world + r, 2*world + r, ...  The chunks of round j from all
+    ranks are the contiguous rows [j*world*s, (j+1)*world*s) of C^T, so one
+    all-gather per round lands every row in place.  rounds=1 is
+    shard_ranges."""
+    if rounds < 1:
+        raise DimensionError(f"rounds must be >= 1, got {rounds}")
+    if n < 0 or world < 1:
+        raise DimensionError(f"bad shard request: N={n}, world={world}")
+    s = -(-n // (world * rounds)) if n else 0
+    return [[(min(n, (j * world + r) * s), min(n, (j * world + r + 1) * s)) for j in range(rounds)]
+            for r in range(world)]
+
+
 class ShardedTwPlan:
     """One rank's share of an N-sharded TW layer.
 
-    gemm_local(at) computes this rank's C^T rows (no communication); gemm(at)
-    also all-gathers the full C^T.  The local block always has
-    rows_per_rank(N, world) rows: rows past the rank's range (only on the
-    last ranks when world does not divide N) are zero."""
+    rounds=1: rank r owns one contiguous column range (shard_ranges).
+    rounds=J>1: block-cyclic chunks (cyclic_ranges); gemm() runs round j's
+    TW-GEMM, then starts round j's all-gather asynchronously, so NCCL moves
+    round j's rows over NVLink while the kernel computes round j+1 --
+    SURVEY.md §8(e)'s overlap by chunking.  Every GEMM writes straight into
+    its slot of the gather buffer and the all-gather runs in place, so the
+    gathered buffer is C^T with no copies.
 
-    def __init__(self, tiles: CompactTileSet, group=None, device=None, dtype=None):
+    gemm_local(at) computes this rank's rows only (no communication) and
+    returns them as a (rounds*chunk, M) view stack; rows past N are zero."""
+
+    def __init__(self, tiles: CompactTileSet, group=None, device=None, dtype=None, rounds: int = 1):
         self.group = group
         self.rank, self.world = _group_info(group)
         self.k, self.n = int(tiles.k), int(tiles.n)
-        self.ranges = shard_ranges(self.n, self.world)
-        self.col_range = self.ranges[self.rank]
-        self.per = rows_per_rank(self.n, self.world)
-        self.plan = TwPlan(tiles, device=device, dtype=dtype, col_range=self.col_range)
-        self.device = self.plan.device
+        self.rounds = int(rounds)
+        self.chunks = cyclic_ranges(self.n, self.world, self.rounds)[self.rank]
+        self.chunk = -(-self.n // (self.world * self.rounds)) if self.n else 0
+        self.ranges = [r[0] for r in cyclic_ranges(self.n, self.world, 1)] if self.rounds == 1 else None
+        self.col_range = self.chunks[0] if self.rounds == 1 else None
+        self.per = self.chunk * self.rounds
+        self.plans = [TwPlan(tiles, device=device, dtype=dtype, col_range=c) if c[1] > c[0] else None
+                      for c in self.chunks]
+        self.plan = next((pl for pl in self.plans if pl is not None), None)
+        self.device = (self.plan.device if self.plan is not None
+                       else torch.device(device) if device is not None
+                       else torch.device("cuda", torch.cuda.current_device()))
         self._bufs: dict = {}
 
     @property
     def info(self):
-        return self.plan.info
+        return [pl.info if pl is not None else None for pl in self.plans]
 
-    def _buffers(self, m: int, out_dtype):
+    def _full(self, m: int, out_dtype):
         key = (m, out_dtype)
         if key not in self._bufs:
-            local = torch.zeros((self.per, m), dtype=out_dtype, device=self.device)
-            full = torch.empty((self.per * self.world, m), dtype=out_dtype, device=self.device)
-            self._bufs[key] = (local, full)
+            # rows past N (tail chunks) stay zero: no GEMM ever writes them
+            self._bufs[key] = torch.zeros((self.chunk * self.world * self.rounds, m), dtype=out_dtype,
+                                          device=self.device)
         return self._bufs[key]
 
+    def _slot(self, full, j):
+        c = j * self.world + self.rank
+        return full[c * self.chunk:(c + 1) * self.chunk]
+
+    def _compute(self, at, full, j, out_dtype, stream):
+        pl, (c0, c1) = self.plans[j], self.chunks[j]
+        if pl is not None:
+            pl.gemm(at, out=self._slot(full, j)[: c1 - c0], out_dtype=out_dtype, stream=stream)
+
     def gemm_local(self, at, out_dtype=None, stream=None):
-        """This rank's C^T rows [c0, c1) (re-based to 0), padded to `per` rows."""
+        """This rank's C^T rows, chunk by chunk ((rounds*chunk) x M)."""
         out_dtype = out_dtype or torch.float32
-        m = at.shape[1]
-        local, _ = self._buffers(m, out_dtype)
-        width = self.col_range[1] - self.col_range[0]
-        if width:
-            self.plan.gemm(at, out=local[:width], out_dtype=out_dtype, stream=stream)
-        return local
+        full = self._full(at.shape[1], out_dtype)
+        for j in range(self.rounds):
+            self._compute(at, full, j, out_dtype, stream)
+        return torch.cat([self._slot(full, j) for j in range(self.rounds)]) if self.rounds > 1 \
+            else self._slot(full, 0)
 
     def gemm(self, at, out_dtype=None, stream=None):
-        """Full C^T (N x M) on every rank: local TW-GEMM + all-gather."""
-        local = self.gemm_local(at, out_dtype, stream)
-        _, full = self._buffers(at.shape[1], local.dtype)
-        return all_gather_rows(local, self.n, self.group, out=full)
+        """Full C^T (N x M) on every rank: per round, TW-GEMM into this
+        rank's slot, then an in-place all-gather of the round's rows.
+        `stream`: a torch.cuda.Stream (or None for the current stream)."""
+        out_dtype = out_dtype or torch.float32
+        full = self._full(at.shape[1], out_dtype)
+        rows = self.world * self.chunk
+        pending = []
+        # NCCL orders each collective after the work queued on the current
+        # stream, so the GEMMs run on it too
+        ctx = torch.cuda.stream(stream) if isinstance(stream, torch.cuda.Stream) else contextlib.nullcontext()
+        with ctx:
+            for j in range(self.rounds):
+                self._compute(at, full, j, out_dtype, None)
+                if self.world > 1:
+                    pending.append(_gather_round(full[j * rows:(j + 1) * rows], self._slot(full, j), self.group))
+            for wk in pending:
+                if wk is not None:
+                    wk.wait()
+        return full[: self.n]
+
+
+def _gather_round(dst, mine, group):
+    """All-gather equal row blocks into `dst`, `mine` being this rank's block
+    inside it (in place).  NCCL: asynchronous, ordered after the GEMM on the
+    current stream.  gloo (host-logic tests): staged through the host."""
+    if mine.is_cuda and dist.get_backend(group) == "nccl":
+        return dist.all_gather_into_tensor(dst, mine, group=group, async_op=True)
+    host = torch.empty(dst.shape, dtype=dst.dtype)
+    dist.all_gather_into_tensor(host, mine.contiguous().cpu(), group=group)
+    dst.copy_(host)
+    return None
 
 
 def shard_table(n: int, world: int) -> np.ndarray:

@@ -294,6 +294,10 @@ def test_sharded_plan_single_rank_equals_full_plan():
     got = sp.gemm(at).cpu().numpy()
     full = tw.TwPlan(ts).gemm(at).cpu().numpy()
     assert np.array_equal(got, full)
+    sp3 = tw.ShardedTwPlan(ts, rounds=3)  # block-cyclic chunks, one plan per round
+    assert sp3.chunks == [(0, 234), (234, 468), (468, 700)]
+    assert np.array_equal(sp3.gemm(at).cpu().numpy(), full)
+    assert np.array_equal(sp3.gemm_local(at)[:700].cpu().numpy(), full)
 
 
 @pytest.mark.parametrize("relu,out_dtype", [(True, torch.float32), (False, torch.float32), (True, torch.float16)])

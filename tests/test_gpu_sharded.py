@@ -18,7 +18,7 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, rounds):
     try:
         import paper_2008_13006_b200 as tw
         from oracle import oracle as orc
@@ -30,12 +30,12 @@ def _worker(rank, world, port, q):
         a, w, p = orc.bench_inputs(384, 512, 1000, 128, 0.75, seed=23)
         ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
         at = torch.from_numpy(np.ascontiguousarray(a.T)).cuda().to(torch.bfloat16)
-        sp = tw.ShardedTwPlan(ts)
+        sp = tw.ShardedTwPlan(ts, rounds=rounds)
         full = sp.gemm(at, out_dtype=torch.float32)
         torch.cuda.synchronize()
         if rank == 0:
             ref = tw.TwPlan(ts).gemm(at).cpu().numpy()
-            q.put(("ok", bool(np.array_equal(full.cpu().numpy(), ref)), sp.col_range, tuple(full.shape)))
+            q.put(("ok", bool(np.array_equal(full.cpu().numpy(), ref)), sp.chunks, tuple(full.shape)))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover
@@ -43,7 +43,8 @@ def _worker(rank, world, port, q):
         raise
 
 
-def test_two_rank_sharded_gemm_on_gpu():
+@pytest.mark.parametrize("rounds", [1, 3])
+def test_two_rank_sharded_gemm_on_gpu(rounds):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     ctx = mp.get_context("spawn")
@@ -51,7 +52,7 @@ def test_two_rank_sharded_gemm_on_gpu():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, rounds)) for r in range(2)]
     for pr in procs:
         pr.start()
     res = q.get(timeout=300)
@@ -59,4 +60,5 @@ def test_two_rank_sharded_gemm_on_gpu():
         pr.join(timeout=120)
     assert res[0] == "ok", res
     assert res[1], "sharded output differs from the single-plan output"
-    assert res[2] == (0, 500) and res[3] == (1000, 384)
+    assert res[2] == ([(0, 500)] if rounds == 1 else [(0, 167), (334, 501), (668, 835)])
+    assert res[3] == (1000, 384)

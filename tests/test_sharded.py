@@ -53,20 +53,37 @@ def emulate_shard(plan: tw.PackedPlan, at32: np.ndarray) -> np.ndarray:
     return ct.astype(np.float32)
 
 
-def _worker(rank, world, port, m, k, n, s, seed, q):
+def _worker(rank, world, port, m, k, n, s, seed, q, rounds=1):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         a, w, p = orc.bench_inputs(m, k, n, 128, s, seed=seed)
         ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
-        c0, c1 = sharded.shard_ranges(n, world)[rank]
-        plan = tw.PackedPlan(ts, col_range=(c0, c1))
-        per = sharded.rows_per_rank(n, world)
-        local = torch.zeros((per, m), dtype=torch.float32)
-        local[: c1 - c0] = torch.from_numpy(emulate_shard(plan, np.ascontiguousarray(a.T)))
-        full = sharded.all_gather_rows(local, n)
+        at32 = np.ascontiguousarray(a.T)
+        kept = torch.zeros(1, dtype=torch.int64)
+        if rounds == 1:
+            c0, c1 = sharded.shard_ranges(n, world)[rank]
+            plan = tw.PackedPlan(ts, col_range=(c0, c1))
+            per = sharded.rows_per_rank(n, world)
+            local = torch.zeros((per, m), dtype=torch.float32)
+            local[: c1 - c0] = torch.from_numpy(emulate_shard(plan, at32))
+            full = sharded.all_gather_rows(local, n)
+            kept += plan.info["kept_elems"]
+        else:
+            # block-cyclic rounds, gathered in place round by round
+            chunks = sharded.cyclic_ranges(n, world, rounds)
+            sz = -(-n // (world * rounds))
+            buf = torch.zeros((sz * world * rounds, m), dtype=torch.float32)
+            for j, (c0, c1) in enumerate(chunks[rank]):
+                c = j * world + rank
+                assert c0 == min(n, c * sz)
+                if c1 > c0:
+                    plan = tw.PackedPlan(ts, col_range=(c0, c1))
+                    buf[c * sz: c * sz + c1 - c0] = torch.from_numpy(emulate_shard(plan, at32))
+                    kept += plan.info["kept_elems"]
+                sharded._gather_round(buf[j * world * sz:(j + 1) * world * sz], buf[c * sz:(c + 1) * sz], None)
+            full = buf[:n]
         assert full.shape == (n, m) and full.is_contiguous()
-        kept = torch.tensor([plan.info["kept_elems"]], dtype=torch.int64)
         dist.all_reduce(kept)
         if rank == 0:
             want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), k, n))
@@ -86,12 +103,27 @@ def _free_port() -> int:
         return sk.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,m,k,n,s", [(2, 96, 256, 1000, 0.75), (3, 64, 200, 700, 0.5)])
-def test_gloo_sharded_layer_reassembles(world, m, k, n, s):
+def test_cyclic_ranges():
+    # 2 ranks x 3 rounds over 1000 columns: chunk 167, rank r owns chunks r, 2+r, 4+r
+    cr = sharded.cyclic_ranges(1000, 2, 3)
+    assert cr[0] == [(0, 167), (334, 501), (668, 835)]
+    assert cr[1] == [(167, 334), (501, 668), (835, 1000)]
+    assert sharded.cyclic_ranges(3072, 8, 1) == [[r] for r in sharded.shard_ranges(3072, 8)]
+    # every column owned exactly once
+    for n, w, j in [(1000, 3, 4), (7, 4, 3), (4096, 8, 4), (0, 2, 2)]:
+        cols = sorted(c for rk in sharded.cyclic_ranges(n, w, j) for a, b in rk for c in range(a, b))
+        assert cols == list(range(n))
+    with pytest.raises(tw.DimensionError):
+        sharded.cyclic_ranges(10, 2, 0)
+
+
+@pytest.mark.parametrize("world,m,k,n,s,rounds", [(2, 96, 256, 1000, 0.75, 1), (3, 64, 200, 700, 0.5, 1),
+                                                  (2, 64, 256, 1000, 0.75, 3)])
+def test_gloo_sharded_layer_reassembles(world, m, k, n, s, rounds):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, m, k, n, s, 7, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, k, n, s, 7, q, rounds)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = q.get(timeout=180)
