@@ -45,7 +45,12 @@ namespace tw {
 
 namespace {
 
-constexpr int kProducerWarps = 4;
+#ifndef TW_PRODUCER_WARPS
+#define TW_PRODUCER_WARPS 4
+#endif
+constexpr int kProducerWarps = TW_PRODUCER_WARPS;
+constexpr int kRowsPerWarp = 64 / kProducerWarps;  // kept rows of a 64-k stage per producer warp
+constexpr int kIdxLanes = kRowsPerWarp / 4;        // lanes that prefetch this warp's row indices
 constexpr int kMmaWarp = kProducerWarps;
 constexpr int kEpiWarp0 = kProducerWarps + 1;
 constexpr int kEpiWarps = 8;
@@ -58,7 +63,7 @@ constexpr int kEpiBarrier = 1;  // named barrier id for the epilogue warps
 // and the record of stage i + kIdxLook into its own shared-memory ring with
 // cp.async while issuing stage i: no register ever waits on an index load.
 constexpr int kIdxInts = 68;
-constexpr int kSlotInts = 20;  // 16 row indices + the 4-int record
+constexpr int kSlotInts = kRowsPerWarp + 4;  // this warp's row indices + the 4-int record
 constexpr int kIdxSlots = 8;
 constexpr int kIdxLook = 4;
 
@@ -357,7 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   const int s_begin = __ldg(args.stream_off + blockIdx.x);
   const int n_st = __ldg(args.stream_off + blockIdx.x + 1) - s_begin;
 
-  if (threadIdx.x == 0) trace_evt(args, 7, 0);  // CTA start
+  if (threadIdx.x == 0) {
+    trace_evt(args, 7, 0);  // CTA start
+    if (args.trace != nullptr) args.trace[((int64_t)blockIdx.x * 8 + 7) * 8 + 2] = (int64_t)clock64();
+  }
   // Programmatic dependent launch: let the next kernel in the stream start
   // its CTAs (they wait in griddepcontrol.wait until this grid completes).
   // This CTA itself only touches immutable plan data (schedule, weights)
@@ -386,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 
   if (warp < kProducerWarps) {
     // ------------------------------------------------ producer warps
-    // Warp w fills kept rows 16w..16w+15 of each 64-row stage.  A row's TB
+    // Warp w fills kept rows w*R..w*R+R-1 (R = kRowsPerWarp) of each 64-row stage.  A row's TB
     // tokens are TB/8 16-byte chunks; one instruction covers 32/(TB/8) rows.
     // Address work per copy is one shuffle of the row's byte offset plus a
     // 64-bit add: the row offsets (kept index * row pitch) are computed once
@@ -404,8 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     int32_t *ring = sIdx + warp * (kIdxSlots * kSlotInts);  // this warp's index ring
     // stage k's 16 row indices of this warp (lanes 0-3) + record (lane 4)
     auto prefetch = [&](int k) {
-      if (lane < 5) {
-        const int32_t *src = args.stream + (int64_t)(s_begin + k) * kIdxInts + (lane < 4 ? warp * 16 + lane * 4 : 64);
+      if (lane <= kIdxLanes) {
+        const int32_t *src =
+            args.stream + (int64_t)(s_begin + k) * kIdxInts + (lane < kIdxLanes ? warp * kRowsPerWarp + lane * 4 : 64);
         ptx::cp_async_16(ring + (k % kIdxSlots) * kSlotInts + lane * 4, src, 16);
       }
     };
@@ -415,16 +424,18 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     }
     // A^T may be produced by the previous kernel in the stream (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    const bool traced = args.trace != nullptr;
     for (int i = 0; i < n_st; ++i) {
       const int32_t *slot = ring + (i % kIdxSlots) * kSlotInts;
-      const long long c0 = clock64();
-      ptx::mbar_wait(&empty[stage], phase ^ 1);
-      const long long c1 = clock64();
+      const long long c0 = traced ? clock64() : 0;  // SM-clock reads only when tracing
+      // 4096 (experiment, needs 4 = no MMA): no back-pressure from the consumer
+      if (!(args.debug & 4096)) ptx::mbar_wait(&empty[stage], phase ^ 1);
+      const long long c1 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       // stage i's indices were the (kIdxLook)-th most recent group
       ptx::cp_async_wait_group<kIdxLook - 1>();
       __syncwarp();
-      const long long c2 = clock64();
-      const int4 rec = *reinterpret_cast<const int4 *>(slot + 16);
+      const long long c2 = traced ? clock64() : 0;  // SM-clock reads only when tracing
+      const int4 rec = *reinterpret_cast<const int4 *>(slot + kRowsPerWarp);
       if (threadIdx.x == 0 && (rec.w & (1 << 16))) trace_evt(args, rec.w & 0xffff, 0);
       const int nh = rec.z & 0xf;
       const bool active = chunk < nh * 16;  // token half present in this unit
@@ -440,33 +451,50 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
           ptx::bulk_g2s(sB + stage * C::kBBytes, args.wimg + rec.x, (uint32_t)args.wbytes, &full[stage], keep);
         }
       }
-      uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + warp * 16 * 128;
+      uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + warp * kRowsPerWarp * 128;
       // all 16 row indices into registers BEFORE the first cp.async: a shared
       // load issued after a cp.async waits for it in the same (MIO) pipe
-      int rows[16];
+      int rows[kRowsPerWarp];
 #pragma unroll
-      for (int v4 = 0; v4 < 4; ++v4) {
+      for (int v4 = 0; v4 < kRowsPerWarp / 4; ++v4) {
         const int4 r4 = reinterpret_cast<const int4 *>(slot)[v4];
         rows[4 * v4] = r4.x; rows[4 * v4 + 1] = r4.y; rows[4 * v4 + 2] = r4.z; rows[4 * v4 + 3] = r4.w;
+      }
+      if (args.debug & 8192) {  // experiment: synthetic rows (random, in range) instead of the kept lists
+#pragma unroll
+        for (int r = 0; r < kRowsPerWarp; ++r) rows[r] = ((warp * kRowsPerWarp + r) * 389 + i * 13 + blockIdx.x * 7) % 768;
       }
       // Fast path (warp-uniform): every row real and the unit's full token
       // range inside M -> plain 16-byte cp.async.  The zero-fill form (with a
       // source-size operand) only for padded rows / ragged token blocks.
       int min_row = rows[0];
 #pragma unroll
-      for (int r = 1; r < 16; ++r) min_row = min(min_row, rows[r]);
+      for (int r = 1; r < kRowsPerWarp; ++r) min_row = min(min_row, rows[r]);
       const bool fast = min_row >= 0 && rec.y + nh * 128 <= args.M && !(args.debug & 256);
-      if (fast) {
+      if (TB == 256 && nh == 1 && fast && !(args.debug & 512)) {
+        // one 128-token half: 256 B per row, so each instruction carries two
+        // rows (lanes 0-15 row 2it, 16-31 row 2it+1) -- half the LDGSTS count
+        // of the one-row form, whose upper 16 lanes would idle
+        const int ch2 = lane & 15, rs2 = lane >> 4, cc2 = ch2 & 7;
+        const char *lb2 = at_bytes + (int64_t)(rec.y + ch2 * 8) * 2;
+        uint8_t *aw2 = sA + stage * C::kABytes + (ch2 >> 3) * 8192 + warp * kRowsPerWarp * 128;
 #pragma unroll
-        for (int it = 0; it < 16 / kRowsPerInst; ++it) {
+        for (int it = 0; it < kRowsPerWarp / 2; ++it) {
+          const int rl = it * 2 + rs2;
+          const int row = rs2 ? rows[2 * it + 1] : rows[2 * it];
+          ptx::cp_async_16_full(aw2 + rl * 128 + ((cc2 ^ (rl & 7)) * 16), lb2 + (int64_t)row * pitch);
+        }
+      } else if (fast) {
+#pragma unroll
+        for (int it = 0; it < kRowsPerWarp / kRowsPerInst; ++it) {
           const int rl = it * kRowsPerInst + rsub;
           const int row = kRowsPerInst == 1 ? rows[it] : (rsub ? rows[it * kRowsPerInst + 1] : rows[it * kRowsPerInst]);
           if (active) ptx::cp_async_16_full(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), lane_base + (int64_t)row * pitch);
         }
       } else {
 #pragma unroll
-        for (int it = 0; it < 16 / kRowsPerInst; ++it) {
-          const int rl = it * kRowsPerInst + rsub;  // row within this warp's 16
+        for (int it = 0; it < kRowsPerWarp / kRowsPerInst; ++it) {
+          const int rl = it * kRowsPerInst + rsub;  // row within this warp's kRowsPerWarp
           const int row = kRowsPerInst == 1 ? rows[it] : (rsub ? rows[it * kRowsPerInst + 1] : rows[it * kRowsPerInst]);
           const uint32_t nbytes = row >= 0 ? src_bytes_m : 0u;
           if (active)
@@ -505,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       // which covers its prefetch of stage i's record into its ring
       ptx::mbar_wait(&full[stage], phase);
       if (lane == 0) trace_stage(args, i, 1);
-      const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kIdxSlots) * kSlotInts + 16);
+      const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kIdxSlots) * kSlotInts + kRowsPerWarp);
       const int nh = rec.z & 0xf, nk = (rec.z >> 4) & 0xf;
       const uint32_t n_mma = (uint32_t)(rec.z >> 8);
       const uint32_t idesc = args.idesc | ((n_mma >> 3) << 17);
@@ -528,7 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
               ptx::mma_f16_ss(d_tmem + h * 128, adesc, bdesc, idesc, (first && kk == 0) ? 0u : 1u);
           }
         }
-        ptx::mma_commit(&empty[stage]);
+        if (args.debug & 16384) ptx::mbar_arrive(&empty[stage]);  // experiment (with 4): plain arrive, no commit
+        else ptx::mma_commit(&empty[stage]);
       }
       __syncwarp();
       if (lane == 0) trace_stage(args, i, 2);
@@ -599,6 +628,13 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       ptx::tc_fence_after();
       epi_sync();  // sCol visible; previous unit's staging reads done
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 5);
+      if (args.debug & 32768) {  // experiment: drop the accumulator unread
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
       const bool mode_a = TB == 256 && nh == 2;
       // 16-bit outputs without accumulate / bias are rounded while staging
       const bool stage16 = sizeof(OutT) == 2 && !args.accumulate && args.bias == nullptr && !(args.debug & 1024);
@@ -677,7 +713,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     for (zr = *s_zdone + e; zr < z1; zr += kEpiWarps)
       zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
     if (lane == 0) ptx::bulk_wait<0>();  // bulk stores performed (and smem read) before exit
-    if (e == 0 && lane == 0) trace_evt(args, 7, 1);  // last zero row issued
+    if (e == 0 && lane == 0) {
+      trace_evt(args, 7, 1);  // last zero row issued
+      if (args.trace != nullptr) args.trace[((int64_t)blockIdx.x * 8 + 7) * 8 + 3] = (int64_t)clock64();
+    }
   }
 
   __syncthreads();

@@ -35,8 +35,11 @@ def main():
     ap.add_argument("--debug", type=int, nargs="+", default=[0, 1, 2, 3, 4, 64])
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warm-a", action="store_true", help="one A^T for every step (L2-resident input)")
+    ap.add_argument("--m", type=int, default=0, help="override the token count M")
+    ap.add_argument("--hot", action="store_true", help="one plan / A^T / output for every step (all L2-resident)")
     args = ap.parse_args()
     m, k, n, g, s, _ = bench.WORKLOADS[args.workload]
+    m = args.m or m
     a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
     ts = tw.compact(tw.DenseMatrix.from_array(w), bench.to_pattern(tw, p))
     dt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[args.out_dtype]
@@ -45,6 +48,8 @@ def main():
     at0 = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
     set_bytes = 2 * k * m + ob * n * m
     n_sets = max(2, int(np.ceil(2 * bench.L2_BYTES / set_bytes)) + 1)
+    if args.hot:
+        n_sets = 1
     plans = [tw.TwPlan(ts) for _ in range(n_sets)]
     ats = [at0] * n_sets if args.warm_a else [at0] + [at0.clone() for _ in range(n_sets - 1)]
     outs = [torch.empty((n, m), dtype=dt, device="cuda") for _ in range(n_sets)]
@@ -58,11 +63,11 @@ def main():
 
     plain = bench.time_device(torch, lambda i: plans[i % n_sets].gemm(ats[i % n_sets], out=outs[i % n_sets],
                                                                      out_dtype=dt), args.steps, n_sets, soak_s=0.5)
-    print(f"{args.workload} {args.out_dtype} plain tw_gemm{' (warm A)' if args.warm_a else ''}: {plain * 1e3:.2f} us")
+    print(f"{args.workload} M={m} {args.out_dtype} plain tw_gemm{' (warm A)' if args.warm_a else ''}{' (hot)' if args.hot else ''}: {plain * 1e3:.2f} us")
     for d in args.debug:
         os.environ["TW_B200_DEBUG"] = str(d)
         ms = bench.time_device(torch, step, args.steps, n_sets, soak_s=0.3)
-        print(f"{args.workload} {args.out_dtype} debug={d:4d}: {ms * 1e3:.2f} us")
+        print(f"{args.workload} M={m} {args.out_dtype} debug={d:4d}: {ms * 1e3:.2f} us")
     os.environ.pop("TW_B200_DEBUG", None)
 
 

@@ -37,8 +37,11 @@ def main():
     ap.add_argument("--json", default=None)
     ap.add_argument("--pad", type=int, default=0, help="extra elements per A^T row (row pitch)")
     ap.add_argument("--cold", action="store_true", help="evict the output from L2 before the traced launch")
+    ap.add_argument("--m", type=int, default=0, help="override the token count M")
+    ap.add_argument("--soak", action="store_true", help="traced launch queued behind ~0.3 s of launches (full clocks)")
     args = ap.parse_args()
     m, k, n, g, s, _ = bench.WORKLOADS[args.workload]
+    m = args.m or m
     a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
     ts = tw.compact(tw.DenseMatrix.from_array(w), bench.to_pattern(tw, p))
     plan = tw.TwPlan(ts)
@@ -59,9 +62,15 @@ def main():
     stream = torch.cuda.current_stream().cuda_stream
     for _ in range(5):
         plan.gemm(at, out=out, out_dtype=dt)
+    torch.cuda.synchronize()
+    # clock soak: ~0.3 s of back-to-back launches, the traced one queued right behind
+    soak = [torch.empty_like(out) for _ in range(4)]
+    for i in range(20000 if args.soak else 0):
+        plan.gemm(at, out=soak[i % 4], out_dtype=dt)
     others = [torch.empty_like(out) for _ in range(5)] if args.cold else []
     ats = [at.clone() for _ in range(5)] if args.cold else []
-    torch.cuda.synchronize()
+    if not args.soak:
+        torch.cuda.synchronize()
     trace.zero_()
     # --cold: back-to-back launches on rotating buffers right before the traced
     # one, with no sync in between (bench.py's steady state)
@@ -74,6 +83,8 @@ def main():
     tr = full[: sms.value * 64].reshape(sms.value, 8, 8)
     st = full[sms.value * 64: sms.value * 192].reshape(sms.value, 32, 4)
     ep = full[sms.value * 192:].reshape(sms.value, 32)
+    tr = tr.copy()
+    tr[:, 7, 2:4] = 0  # clock64 samples, not timestamps
     valid = tr > 0
     t0 = tr[valid].min()
     rel = np.where(valid, (tr - t0) / 1e3, np.nan)  # us
@@ -105,6 +116,12 @@ def main():
     for c in range(8):
         row = [np.nanmedian(erel[:, c * 4 + x]) if np.isfinite(erel[:, c * 4 + x]).any() else float("nan") for x in range(4)]
         print(f"  chunk {c}: " + " ".join(f"{v:8.0f}" for v in row))
+    # SM clock during the launch: clock64 vs globaltimer between CTA start and end
+    ck = full[: sms.value * 64].reshape(sms.value, 8, 8)[:, 7, :4]
+    ok = (ck[:, 0] > 0) & (ck[:, 1] > ck[:, 0]) & (ck[:, 3] > ck[:, 2])
+    if ok.any():
+        mhz = (ck[ok, 3] - ck[ok, 2]) / (ck[ok, 1] - ck[ok, 0]) * 1e3
+        print(f"SM clock during the launch: median {np.median(mhz):.0f} MHz (min {mhz.min():.0f}, max {mhz.max():.0f})")
     ends = rel[:, 7, :3]
     print("CTA start / zeros issued / drained (min med max):",
           [(round(float(np.nanmin(ends[:, i])), 2), round(float(np.nanmedian(ends[:, i])), 2),
