@@ -280,6 +280,35 @@ __device__ __forceinline__ void store_rows16(const GemmArgs &args, OutT *out, co
   if constexpr (sizeof(OutT) != 2) return;  // only instantiated for 16-bit outputs
   const OutT *buf = reinterpret_cast<const OutT *>(buf_f);
   constexpr int PER_ROW = RS / 8;  // 16-byte pieces per staged row (32 | 16)
+  if constexpr (PER_ROW == 16 && kRows % 2 == 0) {
+    // 128-token rows are 256 B: two rows per instruction (lanes 0-15 row
+    // 2j, 16-31 row 2j+1), so no lane idles and the unit's last-chunk drain
+    // issues half as many stores
+    const int half = lane >> 4, piece = lane & 15;
+    uint4 vals2[kRows / 2];
+    int orows2[kRows / 2];
+#pragma unroll
+    for (int j = 0; j < kRows / 2; ++j) {
+      const int srow = r0 + 2 * j + half;
+      const int col = col_of(srow);
+      orows2[j] = (col < n_i && !(args.debug & 2)) ? ucol[col] : -1;
+      vals2[j] = *reinterpret_cast<const uint4 *>(buf + srow * RS + piece * 8);
+    }
+#pragma unroll
+    for (int j = 0; j < kRows / 2; ++j) {
+      if (orows2[j] < 0) continue;
+      OutT *grow = out + (int64_t)orows2[j] * args.ldc + m0 + piece * 8;
+      if (vec && m0 + piece * 8 + 8 <= args.M) {
+        __stcs(reinterpret_cast<uint4 *>(grow), vals2[j]);
+      } else {
+        const uint16_t *hv = reinterpret_cast<const uint16_t *>(&vals2[j]);
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          if (m0 + piece * 8 + x < args.M) reinterpret_cast<uint16_t *>(grow)[x] = hv[x];
+      }
+    }
+    return;
+  }
   uint4 vals[kRows];
   int orows[kRows];
   const bool on = lane < PER_ROW;
