@@ -273,9 +273,10 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.keep_pruned = keep_pruned ? 1 : 0;
   a.wbytes = hp.wrows * 128;
   // kind::f16 instruction descriptor: D f32 [4,6)=1, A/B bf16 [7,10)/[10,13)=1
-  // (fp16 = 0), A MN-major [15]=1, B K-major [16]=0, M=128 -> [24,29)=8.
+  // (fp16 = 0), A (weights) K-major [15]=0, B (gathered A^T) MN-major [16]=1,
+  // M=128 tile columns -> [24,29)=8; N (tokens) is set per unit in the kernel.
   const uint32_t ab = hp.in_dtype == TW_BF16 ? 1u : 0u;
-  a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 15) | ((128u >> 4) << 24);
+  a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 16) | ((128u >> 4) << 24);
   a.block_n = hp.block_n;
   a.trace = trace;
   a.bias = bias;

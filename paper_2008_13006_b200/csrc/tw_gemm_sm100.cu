@@ -11,23 +11,26 @@
 //                                 zeros by the epilogue while it waits for
 //                                 accumulators
 //
-// Work unit = (live tile, token block of nh x 128 tokens).  For tiles of up
-// to 128 columns a unit has up to 256 tokens (two M=128 MMAs per k-step share
-// the weight operand); for G = 256 a unit is 128 tokens x up to 256 columns.
-//   A operand (MN-major, SW128): kept rows of A^T (K x M, M contiguous).  Per
-//     pipeline stage 64 kept k x TB tokens, stored as TB/64 blocks of
-//     [64 rows x 128 B] (8-row swizzle atoms: SBO = 1 KB, blocks LBO = 8 KB).
-//     Gathered by 4 producer warps with 16-byte cp.async (zero fill for
+// Work unit = (live tile, token block of nh x 128 tokens): up to 256 tokens
+// for tiles of up to 128 columns, 128 tokens x up to 256 columns for G = 256.
+// The MMA computes D[tile column][token] = W_tile^T . A^T_kept:
+//   A operand (K-major, SW128): the packed weight image of the tile, one 1-D
+//     TMA bulk copy per stage (wrows x 128 B, pre-swizzled on the host);
+//     M = 128 tile columns (two MMAs for G = 256).
+//   B operand (MN-major, SW128): the kept rows of A^T (K x M, M contiguous).
+//     Per pipeline stage 64 kept k x TB tokens, stored as TB/64 blocks of
+//     [64 rows x 128 B] (8-row swizzle atoms: SBO = 1 KB, blocks LBO = 8 KB),
+//     gathered by 4 producer warps with 16-byte cp.async (zero fill for
 //     padded rows and tokens >= M); completion via cp.async.mbarrier.arrive.
-//   B operand (K-major, SW128): the packed weight image of the tile, one
-//     1-D TMA bulk copy per stage (wrows x 128 B, pre-swizzled on the host).
-//   D (TMEM, fp32): 2 x 256 columns (double buffered accumulators).
-// Epilogue (8 warps).  The output C^T has one row per output column, so a
-// unit's results are token segments of scattered rows.  Storing straight from
-// the TMEM register layout (one token per lane) makes every store
-// instruction hit a different row (1.7-1.9 TB/s in tools/membench2.cu);
-// instead each 32-column chunk is staged through shared memory and written
-// row by row, 16 B per lane, 512 B of one row per warp instruction (4.8 TB/s).
+//     N = the unit's tokens: ONE MMA per k-step for a 256-token unit.
+//   D (TMEM, fp32): lane = tile column, column = token; 2 x 256 columns
+//     (double-buffered accumulators).
+// Epilogue (8 warps, drain_unit).  tcgen05.ld.32x32b gives each thread 32
+// consecutive tokens of one output column, i.e. a piece of one C^T row: the
+// fused bias / ReLU are per-thread constants, the values are rounded once and
+// staged with 16-byte shared stores, and every warp then writes whole C^T row
+// segments with 16-byte streaming stores (storing straight from registers
+// would put 32 rows in every store instruction: 1.3 TB/s in membench2).
 //
 // Warp roles (416 threads): w0-3 producer (A gather + W bulk copy), w4 MMA
 // issuer + TMEM owner, w5-12 epilogue (TMEM lane quadrant = warp % 4).
@@ -152,6 +155,22 @@ __device__ __forceinline__ void unpack16_add(uint4 old, float *v) {
   }
 }
 
+// 16 bytes of S (fp32 x4 or 16-bit x8) -> floats
+template <typename S>
+__device__ __forceinline__ void unpack16(uint4 w, float *y) {
+  const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+  if constexpr (sizeof(S) == 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) y[i] = __uint_as_float(u[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint16_t bits = (uint16_t)(u[i >> 1] >> ((i & 1) * 16));
+      y[i] = cvt_in<S>(*reinterpret_cast<S *>(&bits));
+    }
+  }
+}
+
 // Epilogue value of a pruned output column: 0, or relu?(0 + bias) when the
 // bias/ReLU epilogue is fused (trainer.py:246-248 applies both to every
 // column of the layer output, pruned ones included).
@@ -199,137 +218,116 @@ __device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int la
   }
 }
 
-// Epilogue store phase: this warp's kRows staged rows (starting at staged
-// row r0; staged row r holds tile column col_of(r)) -> their C^T rows, SEG
-// tokens from token m0 (row stride RS floats in the staging buffer).
-template <typename OutT, int kRows, int RS, typename ColOf>
-__device__ __forceinline__ void store_rows(const GemmArgs &args, OutT *out, const float *buf, int r0, int lane, int m0,
-                                           int seg, ColOf col_of, const int32_t *ucol, int n_i, bool vec) {
-  constexpr int V = 16 / (int)sizeof(OutT);
-  constexpr int NIT = (RS / V + 31) / 32;  // 16-byte pieces per lane per row
-  constexpr int kBatch = kRows * NIT * V > 32 ? (32 / (NIT * V) > 0 ? 32 / (NIT * V) : 1) : kRows;
+// Epilogue of one unit (swapped orientation: TMEM lane = tile column, TMEM
+// column = token).  tcgen05.ld.32x32b hands each thread T consecutive tokens
+// of ONE output column -- a piece of one C^T row -- so the bias / ReLU are
+// per-thread constants and staging is 16-byte shared stores of whole row
+// pieces (S = staging type: OutT for 16-bit outputs, rounded once here; fp32
+// for fp32 output and the accumulate mode).  Per pass: TMEM -> registers ->
+// staging [row][RT tokens] (16-byte chunks XOR-swizzled by row: conflict-free
+// both ways) -> one named barrier -> every warp stores whole row segments with
+// 16-byte streaming stores.  The staging buffers are double-buffered by pass
+// parity, and the next pass's TMEM load is issued before this pass's stores.
+//   BN <= 128: one 128-column region; warp (q, h) owns columns 32q..32q+31
+//     and, in every pass, tokens [p*2T + h*T, +T): a staged row holds 2T
+//     contiguous tokens.
+//   BN == 256: region h (columns 128h..128h+127); each warp all tokens.
+template <int BN, typename OutT, typename S, int T>
+__device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, float *sStage, uint32_t t_acc,
+                                           uint64_t *tempty, const TileMeta &t, int m0, int nh, const int32_t *ucol,
+                                           int q, int h, int e, int lane, bool vec) {
+  constexpr int RT = BN <= 128 ? 2 * T : T;          // tokens per staged row per pass
+  constexpr int NROWS = BN <= 128 ? 128 : 256;       // staged rows (tile columns)
+  constexpr int CH = RT * (int)sizeof(S) / 16;       // 16-byte chunks per staged row
+  constexpr int V = 16 / (int)sizeof(OutT);          // output elements per 16-byte store
+  constexpr int LPR = RT / V;                        // lanes per row in the store phase
+  constexpr int RPI = 32 / LPR;                      // rows per store instruction
+  constexpr int WROWS = NROWS / 8;                   // rows stored by each epilogue warp
+  static_assert(T % 32 == 0 && CH % 8 == 0 && 32 % LPR == 0, "epilogue tiling");
+  static_assert(NROWS * RT * (int)sizeof(S) <= 32768, "staging buffer");
+  const int toks = BN <= 128 ? nh * 128 : 128;
+  const int n_pass = (toks + RT - 1) / RT;
+  const int region = BN <= 128 ? 0 : h;
+  const int col = region * 128 + q * 32 + lane;      // tile column of this thread
+  const bool warp_live = region * 128 + q * 32 < t.n_i;
+  const int tw0 = BN <= 128 ? h * T : 0;             // this warp's token offset inside a pass
+  const uint32_t t_base = t_acc + ((uint32_t)(q * 32) << 16) + (uint32_t)(region * 128);
+  float bz = 0.f;
+  if (args.bias != nullptr && col < t.n_i) bz = __ldg(args.bias + ucol[col]);
+  // TMEM sub-chunks of 32 tokens; sub-chunk 0 of pass p + 1 is loaded while
+  // pass p stores (32 registers in flight, as many as the register budget
+  // of the 416-thread CTA allows)
+  auto load = [&](int p, int x, uint32_t (&v)[32]) {
+    const int tau = p * RT + tw0 + 32 * x;
+    if (warp_live && tau < toks) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)tau, v);
+  };
+  uint32_t v[32];
+  load(0, 0, v);
+  for (int p = 0; p < n_pass; ++p) {
+    S *buf = reinterpret_cast<S *>(sStage + (p & 1) * (32768 / 4));
+    const int tau = p * RT + tw0;
+    if (warp_live && tau < toks) {
+      uint4 *row = reinterpret_cast<uint4 *>(buf + col % NROWS * RT);
 #pragma unroll
-  for (int rb0 = 0; rb0 < kRows; rb0 += kBatch) {
-    float vals[kBatch][NIT][V];
-    int orows[kBatch];
+      for (int x = 0; x < T / 32; ++x) {
+        if (x > 0) load(p, x, v);
+        ptx::tmem_ld_wait();
+        // fused bias / ReLU in fp32 (trainer.py:246-248), one rounding to S
+        float f[32];
 #pragma unroll
-    for (int rb = 0; rb < kBatch; ++rb) {
-      const int srow = r0 + rb0 + rb;
-      const int col = col_of(srow);
-      orows[rb] = (col < n_i && !(args.debug & 2)) ? ucol[col] : -1;
-      const float *srow_p = buf + srow * RS;
+        for (int i = 0; i < 32; ++i) {
+          float y = __uint_as_float(v[i]);
+          if (args.bias != nullptr) {
+            y = __fadd_rn(y, bz);
+            if (args.relu) y = fmaxf(y, 0.f);
+          }
+          f[i] = y;
+        }
+        const int c0 = (tw0 + 32 * x) * (int)sizeof(S) / 16;
 #pragma unroll
-      for (int n = 0; n < NIT; ++n) {
-        const int tk = (n * 32 + lane) * V;
-#pragma unroll
-        for (int x = 0; x < V; x += 4) {
-          const float4 f = tk < seg ? *reinterpret_cast<const float4 *>(srow_p + tk + x) : make_float4(0.f, 0.f, 0.f, 0.f);
-          vals[rb][n][x] = f.x; vals[rb][n][x + 1] = f.y; vals[rb][n][x + 2] = f.z; vals[rb][n][x + 3] = f.w;
+        for (int c = 0; c < 32 * (int)sizeof(S) / 16; ++c) {
+          const int cc = c0 + c;
+          row[(cc & ~7) | ((cc ^ col) & 7)] = pack16<S>(f + c * (16 / (int)sizeof(S)));
         }
       }
     }
-#pragma unroll
-    for (int rb = 0; rb < kBatch; ++rb) {
-      if (orows[rb] < 0) continue;
-      OutT *grow = out + (int64_t)orows[rb] * args.ldc + m0;
-      if (args.bias != nullptr) {  // fused bias (+ ReLU): fp32 add then max, as trainer.py:246-248
-        const float bz = __ldg(args.bias + orows[rb]);
-#pragma unroll
-        for (int n = 0; n < NIT; ++n)
-#pragma unroll
-          for (int x = 0; x < V; ++x) {
-            const float z = __fadd_rn(vals[rb][n][x], bz);
-            vals[rb][n][x] = args.relu ? fmaxf(z, 0.f) : z;
-          }
-      }
-#pragma unroll
-      for (int n = 0; n < NIT; ++n) {
-        const int tk = (n * 32 + lane) * V;
-        if (tk >= seg) continue;
-        float *v = vals[rb][n];
-        if (vec && m0 + tk + V <= args.M) {
-          uint4 *p = reinterpret_cast<uint4 *>(grow + tk);
-          if (args.accumulate) unpack16_add<OutT>(*p, v);
-          const uint4 pk = pack16<OutT>(v);
-          if (args.debug & 16) {  // experiment: staging reads without the global store
-            if ((pk.x ^ pk.y ^ pk.z ^ pk.w) == 0x7fc00001u) __stcs(p, pk);
-          } else {
-            __stcs(p, pk);
-          }
-        } else {
-#pragma unroll
-          for (int x = 0; x < V; ++x) {
-            if (m0 + tk + x < args.M) {
-              float r = v[x];
-              if (args.accumulate) r += cvt_in<OutT>(grow[tk + x]);
-              grow[tk + x] = cvt_out<OutT>(r);
-            }
-          }
-        }
-      }
+    if (p == n_pass - 1) {  // every TMEM read of the unit is done: hand the accumulator back
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(tempty);
     }
-  }
-}
-
-// Store phase for 16-bit staging: staged row r already holds the rounded
-// OutT values of tile column col_of(r) (RS tokens, row stride RS); each lane
-// moves 16 bytes (8 tokens) straight from shared to global memory.
-template <typename OutT, int kRows, int RS, typename ColOf>
-__device__ __forceinline__ void store_rows16(const GemmArgs &args, OutT *out, const float *buf_f, int r0, int lane,
-                                             int m0, ColOf col_of, const int32_t *ucol, int n_i, bool vec) {
-  if constexpr (sizeof(OutT) != 2) return;  // only instantiated for 16-bit outputs
-  const OutT *buf = reinterpret_cast<const OutT *>(buf_f);
-  constexpr int PER_ROW = RS / 8;  // 16-byte pieces per staged row (32 | 16)
-  if constexpr (PER_ROW == 16 && kRows % 2 == 0) {
-    // 128-token rows are 256 B: two rows per instruction (lanes 0-15 row
-    // 2j, 16-31 row 2j+1), so no lane idles and the unit's last-chunk drain
-    // issues half as many stores
-    const int half = lane >> 4, piece = lane & 15;
-    uint4 vals2[kRows / 2];
-    int orows2[kRows / 2];
+    epi_sync();  // publishes buf[p & 1]; the stores of pass p - 1 (same buffer at p + 1) are done
+    if (p + 1 < n_pass) load(p + 1, 0, v);
+    // store phase: warp e stores staged rows e*WROWS .. +WROWS, RPI rows per instruction
+    const int lrow = lane / LPR, piece = lane % LPR;
+#pragma unroll 2
+    for (int r0 = 0; r0 < WROWS; r0 += RPI) {
+      const int r = e * WROWS + r0 + lrow;
+      const int c = BN <= 128 ? r : r;  // staged row == tile column
+      const int tk = p * RT + piece * V;  // token within the unit
+      if (c >= t.n_i || (args.debug & 2) || tk >= toks || m0 + tk >= args.M) continue;
+      float y[V];
+      const S *srow = buf + r * RT;
 #pragma unroll
-    for (int j = 0; j < kRows / 2; ++j) {
-      const int srow = r0 + 2 * j + half;
-      const int col = col_of(srow);
-      orows2[j] = (col < n_i && !(args.debug & 2)) ? ucol[col] : -1;
-      vals2[j] = *reinterpret_cast<const uint4 *>(buf + srow * RS + piece * 8);
-    }
-#pragma unroll
-    for (int j = 0; j < kRows / 2; ++j) {
-      if (orows2[j] < 0) continue;
-      OutT *grow = out + (int64_t)orows2[j] * args.ldc + m0 + piece * 8;
-      if (vec && m0 + piece * 8 + 8 <= args.M) {
-        __stcs(reinterpret_cast<uint4 *>(grow), vals2[j]);
+      for (int x = 0; x < V; x += 16 / (int)sizeof(S)) {
+        const int cc = (piece * V + x) * (int)sizeof(S) / 16;
+        const uint4 w = reinterpret_cast<const uint4 *>(srow)[(cc & ~7) | ((cc ^ r) & 7)];
+        unpack16<S>(w, y + x);
+      }
+      OutT *grow = out + (int64_t)ucol[c] * args.ldc + m0 + tk;
+      if (vec && m0 + tk + V <= args.M) {
+        uint4 *gp = reinterpret_cast<uint4 *>(grow);
+        if (args.accumulate) unpack16_add<OutT>(*gp, y);
+        __stcs(gp, pack16<OutT>(y));
       } else {
-        const uint16_t *hv = reinterpret_cast<const uint16_t *>(&vals2[j]);
 #pragma unroll
-        for (int x = 0; x < 8; ++x)
-          if (m0 + piece * 8 + x < args.M) reinterpret_cast<uint16_t *>(grow)[x] = hv[x];
+        for (int x = 0; x < V; ++x) {
+          if (m0 + tk + x < args.M && tk + x < toks) {
+            float z = y[x];
+            if (args.accumulate) z += cvt_in<OutT>(grow[x]);
+            grow[x] = cvt_out<OutT>(z);
+          }
+        }
       }
-    }
-    return;
-  }
-  uint4 vals[kRows];
-  int orows[kRows];
-  const bool on = lane < PER_ROW;
-#pragma unroll
-  for (int rb = 0; rb < kRows; ++rb) {
-    const int srow = r0 + rb;
-    const int col = col_of(srow);
-    orows[rb] = (col < n_i && !(args.debug & 2)) ? ucol[col] : -1;
-    vals[rb] = on ? *reinterpret_cast<const uint4 *>(buf + srow * RS + lane * 8) : make_uint4(0, 0, 0, 0);
-  }
-#pragma unroll
-  for (int rb = 0; rb < kRows; ++rb) {
-    if (orows[rb] < 0 || !on) continue;
-    OutT *grow = out + (int64_t)orows[rb] * args.ldc + m0 + lane * 8;
-    if (vec && m0 + lane * 8 + 8 <= args.M) {
-      __stcs(reinterpret_cast<uint4 *>(grow), vals[rb]);
-    } else {
-      const uint16_t *h = reinterpret_cast<const uint16_t *>(&vals[rb]);
-#pragma unroll
-      for (int x = 0; x < 8; ++x)
-        if (m0 + lane * 8 + x < args.M) reinterpret_cast<uint16_t *>(grow)[x] = h[x];
     }
   }
 }
@@ -351,14 +349,6 @@ __device__ __forceinline__ void trace_stage(const GemmArgs &a, int s, int slot) 
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[(int64_t)gridDim.x * 64 + ((int64_t)blockIdx.x * 32 + s) * 4 + slot] = (int64_t)t;
-  }
-}
-
-// epilogue chunk events of each CTA's first unit (after the stage table)
-// (SM clock cycles, not globaltimer: the intervals are sub-microsecond)
-__device__ __forceinline__ void trace_epi(const GemmArgs &a, int idx) {
-  if (a.trace != nullptr && idx < 32) {
-    a.trace[(int64_t)gridDim.x * 192 + (int64_t)blockIdx.x * 32 + idx] = (int64_t)clock64();
   }
 }
 
@@ -564,8 +554,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (lane == 0) trace_stage(args, i, 1);
       const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kIdxSlots) * kSlotInts + kRowsPerWarp);
       const int nh = rec.z & 0xf, nk = (rec.z >> 4) & 0xf;
-      const uint32_t n_mma = (uint32_t)(rec.z >> 8);
-      const uint32_t idesc = args.idesc | ((n_mma >> 3) << 17);
+      const uint32_t n_tok = BN <= 128 ? (uint32_t)nh * 128u : 128u;  // MMA N = the unit's tokens
+      const uint32_t idesc = args.idesc | ((n_tok >> 3) << 17);
       const bool first = rec.w & (1 << 16), last = rec.w & (1 << 17);
       if (first) {
         d_tmem = tmem_base + (uint32_t)(acc * C::kAccCols);
@@ -576,13 +566,17 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (!(args.debug & 8)) ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
+        // D[tile column][token] += W[column][k] * A^T[k][token]: the weight
+        // block is the K-major A operand (M = 128 columns), the gathered A^T
+        // rows the MN-major B operand (N = the unit's tokens, 64-token SW128
+        // blocks 8 KB apart)
         for (int kk = 0; kk < nk; ++kk) {
-          const uint64_t bdesc = ptx::make_sw128_desc(b_base + stage * C::kBBytes + kk * 32, 16, 1024);
-          for (int h = 0; h < nh; ++h) {
-            const uint64_t adesc =
-                ptx::make_sw128_desc(a_base + stage * C::kABytes + h * 16384 + kk * 2048, 8192, 1024);
+          const uint64_t bdesc = ptx::make_sw128_desc(a_base + stage * C::kABytes + kk * 2048, 8192, 1024);
+#pragma unroll
+          for (int r = 0; r < BN / 128; ++r) {
+            const uint64_t adesc = ptx::make_sw128_desc(b_base + stage * C::kBBytes + r * 16384 + kk * 32, 16, 1024);
             if (!(args.debug & 4))
-              ptx::mma_f16_ss(d_tmem + h * 128, adesc, bdesc, idesc, (first && kk == 0) ? 0u : 1u);
+              ptx::mma_f16_ss(d_tmem + r * 128, adesc, bdesc, idesc, (first && kk == 0) ? 0u : 1u);
           }
         }
         if (args.debug & 16384) ptx::mbar_arrive(&empty[stage]);  // experiment (with 4): plain arrive, no commit
@@ -629,7 +623,6 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // the output may be read / written by the previous kernel (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int z1 = (args.accumulate || args.keep_pruned || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
-    constexpr int CK = C::kChunk;              // 32 accumulator columns per TMEM load
     int acc = 0;
     uint32_t acc_phase = 0;
     OutT *out = reinterpret_cast<OutT *>(args.out);
@@ -660,78 +653,12 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (args.debug & 32768) {  // experiment: drop the accumulator unread
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
-        continue;
-      }
-      const bool mode_a = TB == 256 && nh == 2;
-      // 16-bit outputs without accumulate / bias are rounded while staging
-      const bool stage16 = sizeof(OutT) == 2 && !args.accumulate && args.bias == nullptr && !(args.debug & 1024);
-      const bool mode_c = TB == 256 && nh == 1;
-      const int ccols = mode_c ? 2 * CK : CK;  // tile columns per chunk
-      const int n_chunks = (min(t.n_i, 128) + ccols - 1) / ccols;
-      // first tile column this warp loads for chunk c, and its TMEM column
-      auto warp_col = [&](int c) { return mode_a ? c * CK : (mode_c ? c * ccols + h * CK : h * 128 + c * CK); };
-      auto tmem_col = [&](int c) { return mode_a ? h * 128 + c * CK : warp_col(c); };
-      auto have_chunk = [&](int c) { return warp_col(c) < t.n_i && !(args.debug & 128); };
-      const uint32_t t_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C::kAccCols);
-      uint32_t v[CK];  // TMEM chunk in flight: loaded one chunk ahead of its use
-      if (have_chunk(0)) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)tmem_col(0), v);
-      for (int ci = 0; ci < n_chunks; ++ci) {
-        float *buf = sStage + (ci & 1) * (C::kStageBytes / 4);  // double-buffered staging
-        // 1) TMEM -> registers -> staging: mode A [32 cols][256 tok], modes
-        //    B/C [h][32 cols][128 tok] (conflict-free: consecutive tokens)
-        const bool have = have_chunk(ci);
-        if (have) {
-          ptx::tmem_ld_wait();
-          if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 0);
-          const int rs = mode_a ? 256 : 128;
-          const int so = mode_a ? h * 128 + q * 32 + lane : h * CK * 128 + q * 32 + lane;
-          if (stage16) {  // 16-bit outputs: round once here, stage half the bytes
-            OutT *dst = reinterpret_cast<OutT *>(buf) + so;
-#pragma unroll
-            for (int jj = 0; jj < CK; ++jj) dst[jj * rs] = cvt_out<OutT>(__uint_as_float(v[jj]));
-          } else {
-            float *dst = buf + so;
-#pragma unroll
-            for (int jj = 0; jj < CK; ++jj) dst[jj * rs] = __uint_as_float(v[jj]);
-          }
-        }
-        if (ci == n_chunks - 1) {
-          // all of this warp's TMEM reads for the unit are done: hand the
-          // accumulator back to the MMA warp before storing the last chunk
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&tempty[acc]);
-        }
-        if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 1);
-        // One barrier per chunk: it publishes buf[ci & 1] and (double
-        // buffering) guarantees every warp finished storing chunk ci - 1,
-        // whose buffer chunk ci + 1 will overwrite.
-        epi_sync();
-        // next chunk's TMEM load overlaps this chunk's global stores
-        if (ci + 1 < n_chunks && have_chunk(ci + 1)) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)tmem_col(ci + 1), v);
-        if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 2);
-        // 2) staged rows -> global.  All shared-memory reads of a batch are
-        // issued before its first global store: an LDS queued behind a
-        // backpressured STG in the same pipe would wait for it.
-        if (stage16) {
-          if (mode_a)
-            store_rows16<OutT, 4, 256>(args, out, buf, e * 4, lane, m0, [&](int r) { return ci * CK + r; }, ucol,
-                                       t.n_i, vec);
-          else
-            store_rows16<OutT, 8, 128>(
-                args, out, buf, e * 8, lane, m0,
-                [&](int r) { return mode_c ? ci * ccols + r : (r < CK ? 0 : 128) + ci * CK + (r % CK); }, ucol,
-                t.n_i, vec);
-        } else if (mode_a) {
-          store_rows<OutT, 4, 256>(args, out, buf, e * 4, lane, m0, 256, [&](int r) { return ci * CK + r; }, ucol,
-                                   t.n_i, vec);
-        } else {
-          store_rows<OutT, 8, 128>(args, out, buf, e * 8, lane, m0, 128,
-                                   [&](int r) { return mode_c ? ci * ccols + r : (r < CK ? 0 : 128) + ci * CK + (r % CK); },
-                                   ucol, t.n_i, vec);
-        }
-        if (j == u_begin && e == 0 && lane == 0) trace_epi(args, ci * 4 + 3);
+      } else if (args.accumulate || sizeof(OutT) == 4) {
+        drain_unit<BN, OutT, float, 32>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
+                                         m0, nh, ucol, q, h, e, lane, vec);
+      } else if constexpr (sizeof(OutT) == 2) {
+        drain_unit<BN, OutT, OutT, 64>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
+                                        m0, nh, ucol, q, h, e, lane, vec);
       }
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 6);
       acc ^= 1;
