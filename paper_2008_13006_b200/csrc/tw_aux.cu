@@ -312,6 +312,11 @@ __global__ void __launch_bounds__(kSpmmWarps * 32) spmm_tiled_kernel(const AT *_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mt = m0 + lane * PER;
   for (int64_t jr = j0 + warp; jr < j1; jr += kSpmmWarps) {
+    // accumulating into an existing C^T (gemm_tew): a column without stored
+    // entries leaves its row unchanged -- skip the read-modify-write
+    if (accumulate && (staged ? s_ptr[jr - j0 + 1] == s_ptr[jr - j0]
+                              : __ldg(col_ptr + jr + col_begin + 1) == __ldg(col_ptr + jr + col_begin)))
+      continue;
     float acc[PER];
 #pragma unroll
     for (int x = 0; x < PER; ++x) acc[x] = 0.f;
