@@ -139,8 +139,8 @@ int tw_plan_export(const tw_plan *plan, int which, void *dst, int64_t *bytes);
 /* Host-side view of the static launch schedule tw_gemm would use for M
  * tokens on a GPU with `sms` SMs (per-CTA unit lists + zero-row ranges; the
  * replacement for group_by_shape/execute_batched's LPT bins, engine.py:72-123).
- * which = 0 units (int32 x 4 per unit: live tile, first token, 128-token
- * halves, 0), 1 per-CTA unit offsets (grid + 1), 2 per-CTA zero-row offsets
+ * which = 0 units (int32 x 4 per unit: live tile, first token, 64-token
+ * quarters, 0), 1 per-CTA unit offsets (grid + 1), 2 per-CTA zero-row offsets
  * (grid + 1).  Same size protocol as tw_plan_export. */
 int tw_schedule_export(const tw_plan *plan, int64_t m, int out_dtype, int accumulate, int sms, int which,
                        void *dst, int64_t *bytes);

@@ -11,7 +11,7 @@
 //                                 zeros by the epilogue while it waits for
 //                                 accumulators
 //
-// Work unit = (live tile, token block of nh x 128 tokens): up to 256 tokens
+// Work unit = (live tile, token block of nq x 64 tokens): up to 256 tokens
 // for tiles of up to 128 columns, 128 tokens x up to 256 columns for G = 256.
 // The MMA computes D[tile column][token] = W_tile^T . A^T_kept:
 //   A operand (K-major, SW128): the packed weight image of the tile, one 1-D
@@ -234,7 +234,7 @@ __device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int la
 //   BN == 256: region h (columns 128h..128h+127); each warp all tokens.
 template <int BN, typename OutT, typename S, int T>
 __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, float *sStage, uint32_t t_acc,
-                                           uint64_t *tempty, const TileMeta &t, int m0, int nh, const int32_t *ucol,
+                                           uint64_t *tempty, const TileMeta &t, int m0, int nq, const int32_t *ucol,
                                            int q, int h, int e, int lane, bool vec) {
   constexpr int RT = BN <= 128 ? 2 * T : T;          // tokens per staged row per pass
   constexpr int NROWS = BN <= 128 ? 128 : 256;       // staged rows (tile columns)
@@ -245,7 +245,7 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
   constexpr int WROWS = NROWS / 8;                   // rows stored by each epilogue warp
   static_assert(T % 32 == 0 && CH % 8 == 0 && 32 % LPR == 0, "epilogue tiling");
   static_assert(NROWS * RT * (int)sizeof(S) <= 32768, "staging buffer");
-  const int toks = BN <= 128 ? nh * 128 : 128;
+  const int toks = nq * 64;
   const int n_pass = (toks + RT - 1) / RT;
   const int region = BN <= 128 ? 0 : h;
   const int col = region * 128 + q * 32 + lane;      // tile column of this thread
@@ -456,8 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       const long long c2 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       const int4 rec = *reinterpret_cast<const int4 *>(slot + kRowsPerWarp);
       if (threadIdx.x == 0 && (rec.w & (1 << 16))) trace_evt(args, rec.w & 0xffff, 0);
-      const int nh = rec.z & 0xf;
-      const bool active = chunk < nh * 16;  // token half present in this unit
+      const int nq = rec.z & 0xf;           // 64-token quarters in this unit
+      const bool active = chunk < nq * 8;   // this lane's 8 tokens are in the unit
       const int mcol = rec.y + chunk * 8;
       const uint32_t src_bytes_m =
           !active ? 0u : (mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u));
@@ -489,20 +489,30 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       int min_row = rows[0];
 #pragma unroll
       for (int r = 1; r < kRowsPerWarp; ++r) min_row = min(min_row, rows[r]);
-      const bool fast = min_row >= 0 && rec.y + nh * 128 <= args.M && !(args.debug & 256);
-      if (TB == 256 && nh == 1 && fast && !(args.debug & 512)) {
-        // one 128-token half: 256 B per row, so each instruction carries two
-        // rows (lanes 0-15 row 2it, 16-31 row 2it+1) -- half the LDGSTS count
-        // of the one-row form, whose upper 16 lanes would idle
-        const int ch2 = lane & 15, rs2 = lane >> 4, cc2 = ch2 & 7;
-        const char *lb2 = at_bytes + (int64_t)(rec.y + ch2 * 8) * 2;
-        uint8_t *aw2 = sA + stage * C::kABytes + (ch2 >> 3) * 8192 + warp * kRowsPerWarp * 128;
+      const bool fast = min_row >= 0 && rec.y + nq * 64 <= args.M && !(args.debug & 256);
+      // Units narrower than 256 tokens: R = 4 / nq rows per instruction
+      // (8 * nq lanes per row) so no lane idles -- fewer LDGSTS per stage.
+      auto gather_rows = [&](auto rr) {
+        constexpr int R = decltype(rr)::value;  // rows per instruction
+        constexpr int L = 32 / R;               // 16-byte chunks (lanes) per row
+        const int ch = lane % L, rs = lane / L, cq = ch & 7;
+        const char *lb = at_bytes + (int64_t)(rec.y + ch * 8) * 2;
+        uint8_t *aw = sA + stage * C::kABytes + (ch >> 3) * 8192 + warp * kRowsPerWarp * 128;
 #pragma unroll
-        for (int it = 0; it < kRowsPerWarp / 2; ++it) {
-          const int rl = it * 2 + rs2;
-          const int row = rs2 ? rows[2 * it + 1] : rows[2 * it];
-          ptx::cp_async_16_full(aw2 + rl * 128 + ((cc2 ^ (rl & 7)) * 16), lb2 + (int64_t)row * pitch);
+        for (int it = 0; it < kRowsPerWarp / R; ++it) {
+          const int rl = it * R + rs;
+          int row = rows[it * R];
+#pragma unroll
+          for (int x = 1; x < R; ++x)
+            if (rs == x) row = rows[it * R + x];
+          ptx::cp_async_16_full(aw + rl * 128 + ((cq ^ (rl & 7)) * 16), lb + (int64_t)row * pitch);
         }
+      };
+      const bool narrow = fast && nq * 8 < kChunks && (nq == 1 || nq == 2) && !(args.debug & 512);
+      if (narrow && nq == 2) {
+        gather_rows(std::integral_constant<int, 2>{});
+      } else if (narrow) {
+        gather_rows(std::integral_constant<int, 4>{});
       } else if (fast) {
 #pragma unroll
         for (int it = 0; it < kRowsPerWarp / kRowsPerInst; ++it) {
@@ -553,8 +563,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       ptx::mbar_wait(&full[stage], phase);
       if (lane == 0) trace_stage(args, i, 1);
       const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kIdxSlots) * kSlotInts + kRowsPerWarp);
-      const int nh = rec.z & 0xf, nk = (rec.z >> 4) & 0xf;
-      const uint32_t n_tok = BN <= 128 ? (uint32_t)nh * 128u : 128u;  // MMA N = the unit's tokens
+      const int nq = rec.z & 0xf, nk = (rec.z >> 4) & 0xf;
+      const uint32_t n_tok = (uint32_t)nq * 64u;  // MMA N = the unit's tokens
       const uint32_t idesc = args.idesc | ((n_tok >> 3) << 17);
       const bool first = rec.w & (1 << 16), last = rec.w & (1 << 17);
       if (first) {
@@ -629,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     for (int j = u_begin; j < u_end; ++j) {
       const int4 su = __ldg(args.sched + j);
       const TileMeta t = args.tiles[su.x];
-      const int m0 = su.y, nh = su.z;
+      const int m0 = su.y, nq = su.z;
       // col ids double-buffered by unit parity: a fast warp may fill the next
       // unit's table while others still store this unit's last chunk
       int32_t *ucol = sCol + ((j - u_begin) & 1) * BN;
@@ -655,10 +665,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         ptx::mbar_arrive(&tempty[acc]);
       } else if (args.accumulate || sizeof(OutT) == 4) {
         drain_unit<BN, OutT, float, 32>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
-                                         m0, nh, ucol, q, h, e, lane, vec);
+                                         m0, nq, ucol, q, h, e, lane, vec);
       } else if constexpr (sizeof(OutT) == 2) {
         drain_unit<BN, OutT, OutT, 64>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
-                                        m0, nh, ucol, q, h, e, lane, vec);
+                                        m0, nq, ucol, q, h, e, lane, vec);
       }
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 6);
       acc ^= 1;

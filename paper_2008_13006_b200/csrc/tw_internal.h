@@ -53,7 +53,7 @@ struct HostPlan {
 
 // Static work schedule of one launch shape (plan, M, output width): CTA c
 // runs units[off[c] .. off[c+1]) in order -- each {live tile, first token,
-// number of 128-token halves, 0} -- and writes zero rows
+// number of 64-token quarters, 0} -- and writes zero rows
 // zero_rows[zoff[c] .. zoff[c+1]) in the gaps.  Built on the host by LPT
 // over a byte-cost model (tw_schedule.cpp).
 struct HostSchedule {
@@ -64,7 +64,7 @@ struct HostSchedule {
   // Per-CTA stage streams: stage s of CTA c (s in [soff[c], soff[c+1])) is
   // one 64-k block of one unit: stream[68 s .. 68 s + 64) are its kept A^T
   // row indices (-1 = padding -> zero fill), stream[68 s + 64 .. + 68) the
-  // record {weight-image byte offset, first token, halves | k-steps << 4 |
+  // record {weight-image byte offset, first token, quarters | k-steps << 4 |
   // MMA N << 8, unit-in-CTA | first-block << 16 | last-block << 17}.  The
   // kernel streams it into shared memory with TMA, so the producer's index
   // loads never wait behind its own gathers.

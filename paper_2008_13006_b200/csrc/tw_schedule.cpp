@@ -27,8 +27,9 @@ namespace tw {
 
 namespace {
 
+// nq = the unit's tokens in 64-token quarters (1..4; 1..2 for G = 256)
 struct Unit {
-  int32_t tile, m0, nh;
+  int32_t tile, m0, nq;
   double cost;
 };
 
@@ -37,8 +38,8 @@ constexpr double kReadBps = 90.0;    // bytes / ns / SM
 constexpr double kMmaFlops = 15000;  // flop / ns / SM (8192 flop/clk at ~1.85 GHz)
 constexpr double kFixedNs = 300.0;
 
-double unit_cost(const TileMeta &t, int nh, int ob) {
-  const double toks = 128.0 * nh;
+double unit_cost(const TileMeta &t, int nq, int ob) {
+  const double toks = 64.0 * nq;
   const double out_b = toks * t.n_i * ob;
   const double in_b = (double)t.k_i * (toks * 2.0 + t.n_i * 2.0);
   const double mma = 2.0 * toks * ((t.n_i + 15) / 16 * 16) * (t.k16 * 16.0) / kMmaFlops;
@@ -112,42 +113,44 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
   std::vector<Unit> base;
   for (int32_t t = 0; t < (int32_t)hp.tiles.size(); ++t) {
     for (int64_t m0 = 0; m0 < m; m0 += tb) {
-      const int nh = tb == 256 ? (m - m0 > 128 ? 2 : 1) : 1;
-      base.push_back({t, (int32_t)m0, nh, unit_cost(hp.tiles[(size_t)t], nh, ob)});
+      const int nq = (int)std::min<int64_t>(tb / 64, (m - m0 + 63) / 64);
+      base.push_back({t, (int32_t)m0, nq, unit_cost(hp.tiles[(size_t)t], nq, ob)});
     }
   }
   const int64_t zero_ctas = Z > 0 ? (Z * m * ob + (256 << 10) - 1) / (256 << 10) : 0;
-  // CTAs: enough for every unit -- or every 128-token half-unit, so small
+  // CTAs: enough for every unit -- or every 64-token quarter, so small
   // layers (fewer 256-token units than SMs) can spread over more SMs
-  int64_t halves = 0;
-  for (const Unit &u : base) halves += u.nh;
-  int G = (int)std::min<int64_t>(sms, std::max<int64_t>({halves, zero_ctas, (int64_t)1}));
+  int64_t quarters = 0;
+  for (const Unit &u : base) quarters += u.nq;
+  int G = (int)std::min<int64_t>(sms, std::max<int64_t>({quarters, zero_ctas, (int64_t)1}));
   auto by_cost = [](const Unit &a, const Unit &b) {
     return a.cost != b.cost ? a.cost > b.cost : (a.tile != b.tile ? a.tile < b.tile : a.m0 < b.m0);
   };
   std::stable_sort(base.begin(), base.end(), by_cost);
 
-  // candidate unit sets: as is; 256-token tail units split into halves; all split
+  // Candidate unit sets: as is; the tail (units past the last whole wave)
+  // or everything split into pieces of at most 2 quarters, or of 1 quarter.
+  // A piece re-reads the tile's whole weight block, so smaller pieces only
+  // win where they shorten the makespan -- the cost model decides.
   std::vector<std::vector<Unit>> cands{base};
-  if (tb == 256) {
-    auto split = [&](size_t from) {
-      std::vector<Unit> u(base.begin(), base.begin() + (std::ptrdiff_t)from);
-      for (size_t i = from; i < base.size(); ++i) {
-        const Unit &b = base[i];
-        if (b.nh == 2) {
-          const TileMeta &t = hp.tiles[(size_t)b.tile];
-          u.push_back({b.tile, b.m0, 1, unit_cost(t, 1, ob)});
-          u.push_back({b.tile, b.m0 + 128, 1, unit_cost(t, 1, ob)});
-        } else {
-          u.push_back(b);
-        }
+  auto split = [&](const std::vector<Unit> &from_set, size_t from, int max_nq) {
+    std::vector<Unit> u(from_set.begin(), from_set.begin() + (std::ptrdiff_t)from);
+    for (size_t i = from; i < from_set.size(); ++i) {
+      const Unit &b = from_set[i];
+      const TileMeta &t = hp.tiles[(size_t)b.tile];
+      for (int q = 0; q < b.nq; q += max_nq) {
+        const int nq = std::min(max_nq, b.nq - q);
+        u.push_back({b.tile, b.m0 + 64 * q, nq, unit_cost(t, nq, ob)});
       }
-      std::stable_sort(u.begin(), u.end(), by_cost);
-      return u;
-    };
-    const size_t full = base.size() / (size_t)G * (size_t)G;
-    if (full < base.size() && full > 0) cands.push_back(split(full));
-    cands.push_back(split(0));
+    }
+    std::stable_sort(u.begin(), u.end(), by_cost);
+    return u;
+  };
+  const size_t full = base.size() / (size_t)G * (size_t)G;
+  for (int max_nq : {2, 1}) {
+    if (max_nq >= tb / 64) continue;
+    if (full < base.size() && full > 0) cands.push_back(split(base, full, max_nq));
+    cands.push_back(split(base, 0, max_nq));
   }
   // Pick the candidate with the shortest unit-only makespan (a CTA's units
   // run back to back and their outputs cannot be written before their MMA
@@ -181,7 +184,7 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
   for (int c = 0; c < G; ++c) {
     for (int i : per[(size_t)c]) {
       const Unit &u = units[(size_t)i];
-      s.units.insert(s.units.end(), {u.tile, u.m0, u.nh, 0});
+      s.units.insert(s.units.end(), {u.tile, u.m0, u.nq, 0});
       total += u.cost;
     }
     s.off[(size_t)c + 1] = (int32_t)(s.units.size() / 4);
