@@ -404,3 +404,34 @@ def test_keep_pruned_rows_resident_output():
     x = orc.bench_inputs(96, 384, 8, 8, 0.0, seed=3)[0]
     r1, r2 = net.logits(x), net.logits(x)
     assert np.array_equal(r1, r2)
+
+
+def test_random_triples_sweep_vs_oracle():
+    """test_acceptance.py:63-81's sweep, on the GPU: random (M, K, N) with G in
+    {32, 64, 128, 256} and s in {0, .25, .5, .75, .9} (random_uniform_pattern,
+    the reference's generator) against the C oracle -- rel-L2 within the
+    north_star bar for fp16 output and ~1e-6 for fp32, pruned columns exactly
+    0.  60 seeded cases, small enough for the oracle."""
+    rng = np.random.default_rng(2024)
+    worst16 = worst32 = 0.0
+    for case in range(60):
+        g = int(rng.choice([32, 64, 128, 256]))
+        s = float(rng.choice([0.0, 0.25, 0.5, 0.75, 0.9]))
+        m = int(rng.integers(1, 520))
+        k = int(rng.integers(8, 520))
+        n = int(rng.integers(1, 600))
+        a, w, p = orc.bench_inputs(m, k, n, g, s, seed=1000 + case)
+        ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+        plan = tw.TwPlan(ts)
+        at = device_at(a)
+        want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), k, n),
+                              threads=orc.max_threads())
+        g32 = plan.gemm(at).cpu().numpy()
+        g16 = plan.gemm(at, out_dtype=torch.float16).float().cpu().numpy()
+        pr = orc.pruned_columns(p)
+        assert np.all(g32[pr] == 0.0) and np.all(g16[pr] == 0.0), (case, m, k, n, g, s)
+        if np.abs(want).max() > 0:
+            worst32 = max(worst32, rel_l2(g32, want))
+            worst16 = max(worst16, rel_l2(g16, want))
+    assert worst32 < 1e-5, worst32
+    assert worst16 < RTOL, worst16
