@@ -480,6 +480,18 @@ def run_ours(args):
                               max(3, args.steps // 4), max(3, n_sets), graph=False)
             pipe[f"rounds{rounds}_ms"] = allreduce_max(pms)
             del sp
+        # fused: no collective -- each rank's kernel stores its rows into every
+        # rank's C^T replica through CUDA IPC peer pointers (NVLink P2P)
+        try:
+            sp = tw.ShardedTwPlan(ts, group=None, device=dev, fused=True)
+            barrier()
+            pms = time_device(torch, lambda i: sp.gemm(ats[i % n_sets], out_dtype=out_dt),
+                              max(3, args.steps // 4), max(3, n_sets), graph=False)
+            pipe["fused_peer_store_ms"] = allreduce_max(pms)
+            sp.close()
+            del sp
+        except Exception as exc:  # pragma: no cover - reported, not fatal
+            pipe["fused_peer_store_error"] = repr(exc)[:200]
         result["allgather"]["sharded_gemm_full_output"] = pipe
         # e2e at N GPUs: host fp32 A (pinned) -> H2D + A^T prep -> sharded
         # gemm (fp32, rounds 4) -> D2H of the full C^T on every rank

@@ -180,6 +180,25 @@ int tw_gemm_bias(const tw_plan *plan, const void *at, int64_t m, int64_t lda, vo
 int tw_gemm_ex(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
                int flags, const float *bias, int relu, void *stream);
 
+/* Fused compute + all-gather for the N-sharded layer: the
+ * plan's C^T rows are written to cts[0] (this GPU's full C^T buffer, offset to
+ * the plan's first row) AND to every cts[1 .. n_ct-1] -- the same rows of the
+ * other ranks' C^T replicas, as NVLink peer pointers (tw_ipc_open) -- from
+ * the kernel's epilogue, so the reassembly rides on the stores instead of a
+ * separate ncclAllGather.  No accumulate / bias.  The caller orders the call
+ * against the peers' reads of their replicas (a barrier before and after). */
+#define TW_MAX_PEERS 7
+int tw_gemm_peers(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *const *cts, int n_ct,
+                  int64_t ldc, int out_dtype, void *stream);
+
+/* CUDA IPC for the peer replicas: a device allocation plus its 64-byte
+ * cudaIpcMemHandle_t, opening a peer's handle (peer access enabled lazily),
+ * and the matching releases. */
+int tw_ipc_alloc(int64_t bytes, void **ptr, void *handle);
+int tw_ipc_free(void *ptr);
+int tw_ipc_open(const void *handle, void **ptr);
+int tw_ipc_close(void *ptr);
+
 /* Bit-exact CUDA-core variant of tw_gemm: fp32 multiply then fp32 add, in
  * ascending k per element (exactly mm_accum's rounding sequence); used to
  * prove layouts/indexing independent of tensor-core accumulation order.

@@ -54,6 +54,11 @@ SIGNATURES = {
     "tw_gemm_traced": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _p, _p]),
     "tw_gemm_bias": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _p, _i32, _p]),
     "tw_gemm_ex": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _i32, _p, _i32, _p]),
+    "tw_gemm_peers": (_i32, [_p, _p, _i64, _i64, _p, _i32, _i64, _i32, _p]),
+    "tw_ipc_alloc": (_i32, [_i64, _p, _p]),
+    "tw_ipc_free": (_i32, [_p]),
+    "tw_ipc_open": (_i32, [_p, _p]),
+    "tw_ipc_close": (_i32, [_p]),
     "tw_gemm_exact": (_i32, [_p, _p, _i64, _i64, _p, _i64, _p]),
     "tw_prep_activations": (_i32, [_p, _i64, _i64, _i32, _p, _i64, _i32, _p]),
     "tw_spmm_csc": (_i32, [_p, _i32, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _i32, _i32, _p]),

@@ -197,7 +197,7 @@ int tw_plan_destroy(tw_plan *p) {
 
 static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
                      int out_dtype, int accumulate, int64_t *trace, void *stream, const float *bias = nullptr,
-                     int relu = 0);
+                     int relu = 0, void *const *peers = nullptr, int n_peer = 0);
 
 int tw_gemm(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
             int accumulate, void *stream) {
@@ -219,6 +219,58 @@ int tw_gemm_ex(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *c
                    relu ? 1 : 0);
 }
 
+int tw_gemm_peers(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *const *cts, int n_ct, int64_t ldc,
+                  int out_dtype, void *stream) {
+  clear_error();
+  if (!p || !cts) return fail(TW_ERR_ARG, "null pointer");
+  if (n_ct < 1 || n_ct > 1 + TW_MAX_PEERS) return fail(TW_ERR_ARG, "need 1 .. 1 + TW_MAX_PEERS output replicas");
+  for (int d = 0; d < n_ct; ++d) {
+    if (!cts[d]) return fail(TW_ERR_ARG, "null output replica");
+    if ((reinterpret_cast<uintptr_t>(cts[d]) & 15) != (reinterpret_cast<uintptr_t>(cts[0]) & 15))
+      return fail(TW_ERR_ARG, "output replicas must share their 16-byte alignment");
+  }
+  return gemm_impl(p, at, m, lda, cts[0], ldc, out_dtype, 0, nullptr, stream, nullptr, 0, cts + 1, n_ct - 1);
+}
+
+int tw_ipc_alloc(int64_t bytes, void **ptr, void *handle) {
+  clear_error();
+  if (!ptr || !handle || bytes < 1) return fail(TW_ERR_ARG, "bad ipc allocation request");
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "tw_ipc_alloc cudaMalloc");
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return cuda_fail(e, "cudaIpcGetMemHandle");
+  }
+  std::memcpy(handle, &h, sizeof(h));
+  return TW_OK;
+}
+
+int tw_ipc_free(void *ptr) {
+  clear_error();
+  if (!ptr) return TW_OK;
+  cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? TW_OK : cuda_fail(e, "tw_ipc_free");
+}
+
+int tw_ipc_open(const void *handle, void **ptr) {
+  clear_error();
+  if (!handle || !ptr) return fail(TW_ERR_ARG, "null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? TW_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+int tw_ipc_close(void *ptr) {
+  clear_error();
+  if (!ptr) return TW_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? TW_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
 int tw_gemm_traced(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
                    int64_t *trace, void *stream) {
   if (!trace) return fail(TW_ERR_ARG, "null trace buffer");
@@ -226,7 +278,8 @@ int tw_gemm_traced(const tw_plan *p, const void *at, int64_t m, int64_t lda, voi
 }
 
 static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc,
-                     int out_dtype, int accumulate, int64_t *trace, void *stream, const float *bias, int relu) {
+                     int out_dtype, int accumulate, int64_t *trace, void *stream, const float *bias, int relu,
+                     void *const *peers, int n_peer) {
   clear_error();
   if (!p) return fail(TW_ERR_ARG, "null plan");
   if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan (tw_plan_build_host) cannot run on the GPU");
@@ -281,6 +334,8 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.trace = trace;
   a.bias = bias;
   a.relu = relu;
+  a.n_peer = n_peer;
+  for (int d = 0; d < n_peer; ++d) a.peer[d] = peers[d];
   static const int zero_policy = [] {
     const char *e = std::getenv("TW_B200_ZERO");
     return e ? std::atoi(e) : 0;

@@ -182,27 +182,30 @@ __device__ __forceinline__ float const_row_value(const GemmArgs &a, int row) {
 
 // One constant row (a pruned column of C) written by one warp: coalesced
 // 16-byte streaming stores, 512 B per instruction.
-template <typename OutT>
+template <typename OutT, bool kPeer>
 __device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int lane, bool vec) {
   OutT *base = reinterpret_cast<OutT *>(a.out) + (int64_t)row * a.ldc;
   const int64_t n16 = vec ? (int64_t)a.M * (int64_t)sizeof(OutT) / 16 : 0;
-  uint4 *b16 = reinterpret_cast<uint4 *>(base);
   const float c = const_row_value(a, row);
   float cv[8] = {c, c, c, c, c, c, c, c};
   const uint4 z = pack16<OutT>(cv);
-  for (int64_t i = lane; i < n16; i += 32) __stcs(b16 + i, z);
-  for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) base[i] = cvt_out<OutT>(c);
+  for (int d = -1; d < (kPeer ? a.n_peer : 0); ++d) {  // the local output, then every peer replica
+    OutT *bd = d < 0 ? base : reinterpret_cast<OutT *>(a.peer[d]) + (int64_t)row * a.ldc;
+    uint4 *b16d = reinterpret_cast<uint4 *>(bd);
+    for (int64_t i = lane; i < n16; i += 32) __stcs(b16d + i, z);
+    for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) bd[i] = cvt_out<OutT>(c);
+  }
 }
 
 // One zero row by 1-D TMA bulk stores (up to 8 KB each) from the zeroed smem
 // block, issued by lane 0: zero rows never occupy the LSU that the gathers
 // need (tools/membench7.cu: 8 KB bulk stores reach 5.4 TB/s chip-wide).
 // Falls back to STG when the row is not 16-byte aligned / sized.
-template <typename OutT>
+template <typename OutT, bool kPeer>
 __device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int lane, bool bulk_ok, bool vec,
                                               const uint8_t *zero_buf, uint32_t zero_bytes) {
-  if (!bulk_ok || (a.bias != nullptr && const_row_value(a, row) != 0.f)) {
-    write_zero_row<OutT>(a, row, lane, vec);
+  if (!bulk_ok || kPeer || (a.bias != nullptr && const_row_value(a, row) != 0.f)) {
+    write_zero_row<OutT, kPeer>(a, row, lane, vec);
     return;
   }
   if (lane == 0) {
@@ -232,7 +235,7 @@ __device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int la
 //     and, in every pass, tokens [p*2T + h*T, +T): a staged row holds 2T
 //     contiguous tokens.
 //   BN == 256: region h (columns 128h..128h+127); each warp all tokens.
-template <int BN, typename OutT, typename S, int T>
+template <int BN, typename OutT, typename S, int T, bool kPeer>
 __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, float *sStage, uint32_t t_acc,
                                            uint64_t *tempty, const TileMeta &t, int m0, int nq, const int32_t *ucol,
                                            int q, int h, int e, int lane, bool vec) {
@@ -313,11 +316,18 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
         const uint4 w = reinterpret_cast<const uint4 *>(srow)[(cc & ~7) | ((cc ^ r) & 7)];
         unpack16<S>(w, y + x);
       }
-      OutT *grow = out + (int64_t)ucol[c] * args.ldc + m0 + tk;
+      const int64_t off = (int64_t)ucol[c] * args.ldc + m0 + tk;
+      OutT *grow = out + off;
       if (vec && m0 + tk + V <= args.M) {
         uint4 *gp = reinterpret_cast<uint4 *>(grow);
         if (args.accumulate) unpack16_add<OutT>(*gp, y);
-        __stcs(gp, pack16<OutT>(y));
+        const uint4 pk = pack16<OutT>(y);
+        __stcs(gp, pk);
+        // fused all-gather: the same 16 bytes into every peer's replica of
+        // C^T (NVLink peer stores; tw_gemm_peers)
+        if constexpr (kPeer)
+          for (int d = 0; d < args.n_peer; ++d)
+            __stcs(reinterpret_cast<uint4 *>(reinterpret_cast<OutT *>(args.peer[d]) + off), pk);
       } else {
 #pragma unroll
         for (int x = 0; x < V; ++x) {
@@ -325,6 +335,8 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
             float z = y[x];
             if (args.accumulate) z += cvt_in<OutT>(grow[x]);
             grow[x] = cvt_out<OutT>(z);
+            if constexpr (kPeer)
+              for (int d = 0; d < args.n_peer; ++d) reinterpret_cast<OutT *>(args.peer[d])[off + x] = cvt_out<OutT>(z);
           }
         }
       }
@@ -352,7 +364,7 @@ __device__ __forceinline__ void trace_stage(const GemmArgs &a, int s, int slot) 
   }
 }
 
-template <int BN, typename OutT>
+template <int BN, typename OutT, bool kPeer>
 __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid_constant__ GemmArgs args) {
   using C = Cfg<BN>;
   constexpr int TB = C::TB;
@@ -653,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         if (lane == 0 && bulk_ok) {
           if (args.debug & 2048) ptx::bulk_wait_read<2>(); else ptx::bulk_wait_read<0>();
         }
-        zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
+        zero_row_bulk<OutT, kPeer>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
         ++zr;
       }
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -664,10 +676,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
       } else if (args.accumulate || sizeof(OutT) == 4) {
-        drain_unit<BN, OutT, float, 32>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
+        drain_unit<BN, OutT, float, 32, kPeer>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
                                          m0, nq, ucol, q, h, e, lane, vec);
       } else if constexpr (sizeof(OutT) == 2) {
-        drain_unit<BN, OutT, OutT, 64>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
+        drain_unit<BN, OutT, OutT, 64, kPeer>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
                                         m0, nq, ucol, q, h, e, lane, vec);
       }
       if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 6);
@@ -677,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     if (e == 0 && lane == 0) *s_zdone = zr;
     epi_sync();
     for (zr = *s_zdone + e; zr < z1; zr += kEpiWarps)
-      zero_row_bulk<OutT>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
+      zero_row_bulk<OutT, kPeer>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
     if (lane == 0) ptx::bulk_wait<0>();  // bulk stores performed (and smem read) before exit
     if (e == 0 && lane == 0) {
       trace_evt(args, 7, 1);  // last zero row issued
@@ -692,9 +704,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   }
 }
 
-template <int BN, typename OutT>
+template <int BN, typename OutT, bool kPeer>
 cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
-  auto kern = tw_gemm_sm100_kernel<BN, OutT>;
+  auto kern = tw_gemm_sm100_kernel<BN, OutT, kPeer>;
   const int smem = (int)Cfg<BN>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -721,7 +733,13 @@ cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
 
 template <typename OutT>
 cudaError_t launch_out(const GemmArgs &args, int grid, cudaStream_t stream) {
-  return args.block_n <= 128 ? launch_bn<128, OutT>(args, grid, stream) : launch_bn<256, OutT>(args, grid, stream);
+  // peer-store variant (tw_gemm_peers) only when there are replicas: the
+  // extra store loop costs the plain kernel registers and ~1 us at C2a
+  if (args.n_peer > 0)
+    return args.block_n <= 128 ? launch_bn<128, OutT, true>(args, grid, stream)
+                               : launch_bn<256, OutT, true>(args, grid, stream);
+  return args.block_n <= 128 ? launch_bn<128, OutT, false>(args, grid, stream)
+                             : launch_bn<256, OutT, false>(args, grid, stream);
 }
 
 }  // namespace

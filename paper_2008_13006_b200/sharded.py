@@ -20,6 +20,7 @@ NVLink/NVSwitch on a B200 box, gloo for the CPU tests of the host logic).
 from __future__ import annotations
 
 import contextlib
+import ctypes
 
 import numpy as np
 
@@ -30,7 +31,8 @@ except ImportError:  # pragma: no cover
     torch = None
     dist = None
 
-from .engine import TwPlan
+from . import _lib
+from .engine import TwPlan, _code, _stream_ptr
 from .matrix import DimensionError
 from .pattern import CompactTileSet
 
@@ -112,9 +114,14 @@ class ShardedTwPlan:
     gemm_local(at) computes this rank's rows only (no communication) and
     returns them as a (rounds*chunk, M) view stack; rows past N are zero."""
 
-    def __init__(self, tiles: CompactTileSet, group=None, device=None, dtype=None, rounds: int = 1):
+    def __init__(self, tiles: CompactTileSet, group=None, device=None, dtype=None, rounds: int = 1,
+                 fused: bool = False):
         self.group = group
         self.rank, self.world = _group_info(group)
+        if fused and rounds != 1:
+            raise DimensionError("the fused (peer-store) all-gather uses contiguous ranges: rounds must be 1")
+        self.fused = bool(fused)
+        self._peer: dict = {}
         self.k, self.n = int(tiles.k), int(tiles.n)
         self.rounds = int(rounds)
         self.chunks = cyclic_ranges(self.n, self.world, self.rounds)[self.rank]
@@ -160,11 +167,76 @@ class ShardedTwPlan:
         return torch.cat([self._slot(full, j) for j in range(self.rounds)]) if self.rounds > 1 \
             else self._slot(full, 0)
 
+    def _peer_buffers(self, m: int, out_dtype):
+        """Fused mode: every rank's full C^T buffer is a CUDA IPC allocation;
+        the handles are exchanged once over the process group and opened, so
+        this rank's kernel can store its rows into all replicas."""
+        key = (m, out_dtype)
+        if key in self._peer:
+            return self._peer[key]
+        esize = torch.tensor([], dtype=out_dtype).element_size()
+        rows = self.per * self.world
+        nbytes = max(1, rows * m * esize)
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        _lib.call("tw_ipc_alloc", nbytes, ctypes.byref(ptr), ctypes.cast(handle, ctypes.c_void_p))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=self.group)
+        ptrs = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(ptr.value)
+            else:
+                pp = ctypes.c_void_p()
+                hb = (ctypes.c_char * 64).from_buffer_copy(h)
+                _lib.call("tw_ipc_open", ctypes.cast(hb, ctypes.c_void_p), ctypes.byref(pp))
+                ptrs.append(pp.value)
+        full = _device_view(ptr.value, (rows, m), out_dtype, self.device)
+        full.zero_()  # rows past N stay zero
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        # this rank's rows inside every replica: the local one first
+        row0 = self.col_range[0] * m * esize
+        order = [self.rank] + [r for r in range(self.world) if r != self.rank]
+        dsts = (ctypes.c_void_p * self.world)(*[ptrs[r] + row0 for r in order])
+        self._peer[key] = (full, dsts, ptr.value, [ptrs[r] for r in range(self.world) if r != self.rank])
+        return self._peer[key]
+
+    def close(self):
+        """Release the fused mode's IPC buffers (after a barrier: peers may
+        still be storing into this rank's replica otherwise)."""
+        if self._peer and dist is not None and dist.is_initialized():
+            dist.barrier(group=self.group)
+        for full, _dsts, own, peers in self._peer.values():
+            for pp in peers:
+                _lib.call("tw_ipc_close", pp)
+            _lib.call("tw_ipc_free", own)
+        self._peer.clear()
+
+    def _gemm_fused(self, at, out_dtype, stream):
+        m = at.shape[1]
+        full, dsts, _own, _peers = self._peer_buffers(m, out_dtype)
+        width = self.col_range[1] - self.col_range[0]
+        # peers are done reading the previous result from their replicas
+        dist.barrier(group=self.group)
+        if width and m:
+            if at.dtype != self.plan.dtype or at.dim() != 2 or at.shape[0] != self.k:
+                raise DimensionError(f"A^T must be a ({self.k}, M) {self.plan.dtype} CUDA tensor")
+            _lib.call("tw_gemm_peers", self.plan._h, at.data_ptr(), m, at.stride(0), ctypes.cast(dsts, ctypes.c_void_p),
+                      self.world, m,
+                      _code(out_dtype), _stream_ptr(stream))
+        # every rank's rows have landed in every replica
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        return full[: self.n]
+
     def gemm(self, at, out_dtype=None, stream=None):
         """Full C^T (N x M) on every rank: per round, TW-GEMM into this
         rank's slot, then an in-place all-gather of the round's rows.
         `stream`: a torch.cuda.Stream (or None for the current stream)."""
         out_dtype = out_dtype or torch.float32
+        if self.fused and self.world > 1:
+            return self._gemm_fused(at, out_dtype, stream)
         full = self._full(at.shape[1], out_dtype)
         rows = self.world * self.chunk
         pending = []
@@ -180,6 +252,20 @@ class ShardedTwPlan:
                 if wk is not None:
                     wk.wait()
         return full[: self.n]
+
+
+class _CudaArray:
+    """__cuda_array_interface__ wrapper: a torch view of a raw device buffer."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _device_view(ptr, shape, dtype, device):
+    typestr = {torch.float32: "<f4", torch.float16: "<f2", torch.bfloat16: "<f2"}[dtype]
+    t = torch.as_tensor(_CudaArray(ptr, shape, typestr), device=device)
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
 
 
 def _gather_round(dst, mine, group):

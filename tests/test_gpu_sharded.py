@@ -18,7 +18,7 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, q, rounds):
+def _worker(rank, world, port, q, rounds, fused=False):
     try:
         import paper_2008_13006_b200 as tw
         from oracle import oracle as orc
@@ -30,21 +30,25 @@ def _worker(rank, world, port, q, rounds):
         a, w, p = orc.bench_inputs(384, 512, 1000, 128, 0.75, seed=23)
         ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
         at = torch.from_numpy(np.ascontiguousarray(a.T)).cuda().to(torch.bfloat16)
-        sp = tw.ShardedTwPlan(ts, rounds=rounds)
+        sp = tw.ShardedTwPlan(ts, rounds=rounds, fused=fused)
         full = sp.gemm(at, out_dtype=torch.float32)
+        full = sp.gemm(at, out_dtype=torch.float32).clone()  # second call reuses the replicas
         torch.cuda.synchronize()
         if rank == 0:
             ref = tw.TwPlan(ts).gemm(at).cpu().numpy()
             q.put(("ok", bool(np.array_equal(full.cpu().numpy(), ref)), sp.chunks, tuple(full.shape)))
         dist.barrier()
+        sp.close()
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover
         q.put(("err", repr(e)))
         raise
 
 
-@pytest.mark.parametrize("rounds", [1, 3])
-def test_two_rank_sharded_gemm_on_gpu(rounds):
+@pytest.mark.parametrize("rounds,fused", [(1, False), (3, False), (1, True)])
+def test_two_rank_sharded_gemm_on_gpu(rounds, fused):
+    """fused=True: no collective -- each rank's kernel stores its rows into both
+    ranks' C^T replicas through CUDA IPC peer pointers (tw_gemm_peers)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     ctx = mp.get_context("spawn")
@@ -52,7 +56,7 @@ def test_two_rank_sharded_gemm_on_gpu(rounds):
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, rounds)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, rounds, fused)) for r in range(2)]
     for pr in procs:
         pr.start()
     res = q.get(timeout=300)

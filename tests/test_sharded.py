@@ -135,3 +135,12 @@ def test_gloo_sharded_layer_reassembles(world, m, k, n, s, rounds):
     assert zeros_ok
     assert kept == kept_want
     assert all(pr.exitcode == 0 for pr in procs)
+
+
+def test_fused_mode_needs_contiguous_ranges():
+    # the peer-store (fused all-gather) path writes each rank's contiguous
+    # column range into every replica; block-cyclic rounds are rejected
+    a, w, p = orc.bench_inputs(16, 64, 256, 128, 0.5, seed=3)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    with pytest.raises(tw.DimensionError):
+        sharded.ShardedTwPlan(ts, rounds=2, fused=True)
