@@ -73,12 +73,47 @@ class TwMlp:
                 at = plan.gemm(at, out_dtype=torch.float32, bias=b, relu=False, stream=stream)
         return at
 
+    def graph(self, m: int) -> "TwMlpGraph":
+        """Capture the whole forward for M tokens into one CUDA graph (the
+        serving path: at small M the layer chain is launch-bound).  One eager
+        pass first builds the launch schedules and writes the resident
+        activations' pruned rows; the captured pass then writes kept rows only
+        (write_pruned=False), with bias/ReLU fused, layer to layer in HBM."""
+        k0 = self.plans[0].k
+        ld = (m + 7) // 8 * 8
+        static_in = torch.zeros((k0, ld), dtype=self.dtype, device=self.device)[:, :m]
+        self.forward_t(static_in)
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            self.forward_t(static_in)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            static_out = self.forward_t(static_in)
+        return TwMlpGraph(g, static_in, static_out)
+
     def logits(self, x) -> np.ndarray:
         """x: M x K0 (host) -> M x N_last fp32 (host), like engine_logits."""
         x = np.ascontiguousarray(np.asarray(x, np.float32))
         xt = torch.from_numpy(x).to(self.device)
         at = prep_activations(xt, Layout.ROW_MAJOR, self.dtype)
         return self.forward_t(at).t().contiguous().cpu().numpy()
+
+
+class TwMlpGraph:
+    """A captured TwMlp forward: write A^T into `.input` (K0 x M, plan dtype)
+    or pass it to __call__, replay, read `.output` (N_last x M, fp32)."""
+
+    def __init__(self, graph, static_in, static_out):
+        self._g, self.input, self.output = graph, static_in, static_out
+
+    def __call__(self, at=None):
+        if at is not None:
+            self.input.copy_(at)
+        self._g.replay()
+        return self.output
 
 
 def engine_logits(model, x, patterns, workers: int = 1, *, device=None, dtype=None) -> np.ndarray:

@@ -435,3 +435,23 @@ def test_random_triples_sweep_vs_oracle():
             worst16 = max(worst16, rel_l2(g16, want))
     assert worst32 < 1e-5, worst32
     assert worst16 < RTOL, worst16
+
+
+def test_mlp_cuda_graph_replay_matches_eager():
+    """TwMlp.graph(M): the captured layer chain (resident activations, kept
+    rows only) replays to exactly the eager forward's logits, for new inputs
+    written into the static input buffer."""
+    rng = np.random.default_rng(5)
+    dims = [256, 384, 256, 64]
+    ws = [rng.standard_normal((dims[i], dims[i + 1])).astype(np.float32) * 0.1 for i in range(3)]
+    bs = [rng.standard_normal(dims[i + 1]).astype(np.float32) * 0.1 for i in range(3)]
+    ps = [to_tw_pattern(orc.random_uniform_pattern(dims[i], dims[i + 1], 128, 0.75, seed=i)) for i in range(3)]
+    net = tw.TwMlp(ws, bs, ps)
+    graphed = net.graph(200)
+    for seed in range(3):
+        x = np.random.default_rng(seed).standard_normal((200, 256)).astype(np.float32)
+        at = tw.prep_activations(torch.from_numpy(x).cuda(), tw.Layout.ROW_MAJOR, torch.float16)
+        eager = net.forward_t(at).clone()
+        got = graphed(at)
+        torch.cuda.synchronize()
+        assert torch.equal(got, eager)
