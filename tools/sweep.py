@@ -50,7 +50,8 @@ VGG = [  # (name, H, Cin, Cout)
 
 def rows(quick: bool):
     r = [("C1", 1024, 1024, 1024, 0.50, None), ("C2a", 4096, 768, 3072, 0.75, None),
-         ("C2b", 4096, 768, 768, 0.75, None), ("C4-TEW", 4096, 768, 3072, 0.765, 0.015)]
+         ("C2b", 4096, 768, 768, 0.75, None), ("C4-TEW", 4096, 768, 3072, 0.765, 0.015),
+         ("C2a-het", 4096, 768, 3072, 0.75, None), ("C5-het@0.75", 16384, 1024, 4096, 0.75, None)]
     for s in ([0.0, 0.5, 0.75, 0.9] if quick else [0.0, 0.1, 0.25, 0.5, 0.75, 0.9]):
         r.append((f"C5@{s:g}", 16384, 1024, 4096, s, None))
     vgg = VGG[1::3] if quick else VGG
@@ -77,6 +78,17 @@ def run_row(name, m, k, n, s, delta, reps, hbm_peak):
     rng = np.random.default_rng(42)
     w = orc.bf16_round(rng.standard_normal((k, n)).astype(np.float32))
     p = orc.random_uniform_pattern(k, n, g, s, 42)
+    if "-het" in name:
+        # non-uniform tiles: each tile keeps k_i = kbar * U(0.85, 1.15)
+        # rows, so units differ in cost and the LPT schedule has to balance them
+        hr = np.random.default_rng(7)
+        tiles = []
+        for cols, keep in p[3]:
+            kk = int(np.clip(round(keep.sum() * hr.uniform(0.85, 1.15)), 1, k))
+            nk = np.zeros(k, bool)
+            nk[np.sort(hr.choice(k, size=kk, replace=False))] = True
+            tiles.append((cols, nk))
+        p = (p[0], p[1], p[2], tiles)
     ts = tw.compact(tw.DenseMatrix.from_array(w), bench.to_pattern(tw, p))
     plan = tw.TwPlan(ts)
     info = plan.info
