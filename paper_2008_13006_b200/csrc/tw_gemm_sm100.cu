@@ -73,14 +73,11 @@ constexpr int kIdxLook = 4;
 template <int BN>
 struct Cfg {
   static constexpr int TB = BN <= 128 ? 256 : 128;           // max tokens per unit
-  static constexpr int kHalves = TB / 128;                    // max M=128 MMAs per k-step
-  static constexpr uint32_t kABytes = TB * kBlockK * 2;       // 32 KB | 16 KB
-  static constexpr uint32_t kBBytes = BN * 128;               // 16 KB | 32 KB
+  static constexpr uint32_t kABytes = TB * kBlockK * 2;       // gathered A^T rows per stage: 32 KB | 16 KB
+  static constexpr uint32_t kBBytes = BN * 128;               // weight block per stage: 16 KB | 32 KB
   static constexpr uint32_t kAccCols = 256;                   // TMEM columns per accumulator
   static constexpr uint32_t kTmemCols = 2 * kAccCols;
-  static constexpr int kChunk = 32;                           // accumulator columns per epilogue chunk
-  static constexpr int kStageCols = kHalves == 2 ? kChunk : 2 * kChunk;  // staged C^T rows per chunk
-  static constexpr uint32_t kStageBytes = kStageCols * TB * 4;          // 16 KB; two are used
+  static constexpr uint32_t kStageBytes = 32768;              // epilogue staging pass buffer; two are used
   static constexpr uint32_t kColBytes = 2 * BN * 4;                     // col-id table, double buffered
   static constexpr uint32_t kZeroBytes = 8192;  // zero source block for TMA zero-row stores
   static constexpr uint32_t kFixed = 1024 /*align slack*/ + 2 * kStageBytes + kColBytes + 256 /*barriers*/ +
@@ -617,15 +614,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     }
   } else {
     // ------------------------------------------------ epilogue (8 warps)
-    // Warp e reads TMEM lane quadrant q = warp % 4 (tokens 32q..32q+31 of a
-    // 128-token half); the warp pairs (e, e + 4) split the rest by `h`:
-    //   mode A (TB = 256, two token halves): h = token half, 32-column chunks;
-    //   mode B (TB = 128, G = 256):          h = 128-column half, 32-col chunks;
-    //   mode C (TB = 256, one token half):   h = which 32 columns of a 64-column
-    //                                         chunk -- all 8 warps stay busy.
-    // Per chunk: tcgen05.ld (issued one chunk ahead) -> staging [row][token]
-    // in smem -> each warp stores whole C^T row segments with 16-byte
-    // streaming stores (512 B of one row per instruction).
+    // Warp e reads TMEM lane quadrant q = warp % 4 (tile columns 32q..32q+31
+    // of a 128-column region); the warp pairs (e, e + 4) split the rest by
+    // h = e / 4: token halves of every staging pass (G <= 128) or the two
+    // 128-column regions (G = 256).  drain_unit does the per-unit work.
     const int e = warp - kEpiWarp0;   // 0..7
     const int et = e * 32 + lane;     // 0..255
     const int q = warp & 3;
