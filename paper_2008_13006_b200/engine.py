@@ -28,7 +28,8 @@ import numpy as np
 
 from . import _lib
 from .matrix import CscMatrix, DenseMatrix, DimensionError, Layout, as_csc, as_dense
-from .pattern import CompactTileSet, _flatten_tiles, compact, dense_pattern
+from .pattern import (CompactTile, CompactTileSet, _flatten_tiles, compact, dense_pattern, pack_mask_words,
+                      unpack_mask_words)
 
 try:
     import torch
@@ -101,6 +102,7 @@ class PackedPlan:
         else:
             k, n, g, c0, c1, col_off, col_ids, words, subs, sub_off = _plan_args(tiles, col_range)
             n_tiles = len(tiles.tiles)
+        self._tiles = tiles  # host tile set (for derived plans: gemm_tew's merged plan)
         self.k, self.n, self.g, self.col_begin, self.col_end = k, n, g, c0, c1
         self.in_code = {"bf16": _lib.TW_BF16, "fp16": _lib.TW_F16}[dtype]
         handle = ctypes.c_void_p()
@@ -256,12 +258,29 @@ class TwPlan(PackedPlan):
                   _stream_ptr(stream))
         return ct
 
-    def gemm_tew(self, at, csc: "DeviceCsc", out=None, out_dtype=None, stream=None):
-        """engine.py:184-198: TW + element-wise CSC overlay (all N columns)."""
+    def gemm_tew(self, at, csc: "DeviceCsc", out=None, out_dtype=None, stream=None, merged=True):
+        """engine.py:184-198: TW + element-wise CSC overlay (all N columns).
+
+        merged=True (default, the B200 path): ONE persistent TW-GEMM over a
+        plan whose tiles carry the overlay too (tew_merged_tileset): each
+        tile's kept-K list grows by the overlay rows of its columns and its
+        weights gain the overlay values; the overlay entries of pruned
+        columns form extra tiles.  The tensor cores absorb the residual, and
+        there is no second pass over C^T.  merged=False: the reference's
+        composition, TW-GEMM then the CSC SpMM accumulated into the same
+        output (tw_gemm_tew)."""
         out_dtype = out_dtype or torch.float32
         m, lda = self._check_at(at)
         if csc.rows != self.k or csc.cols != self.n:
             raise DimensionError(f"overlay is {csc.rows}x{csc.cols}, pattern is {self.k}x{self.n}")
+        if merged and csc.nnz > 0 and getattr(self, "_tiles", None) is not None and csc.host is not None:
+            cache = self.__dict__.setdefault("_tew_plans", {})
+            key = id(csc)
+            if key not in cache or cache[key][0] is not csc:
+                ts = tew_merged_tileset(self._tiles, csc.host)
+                cache[key] = (csc, TwPlan(ts, device=self.device, dtype=self.dtype,
+                                          col_range=(self.col_begin, self.col_end)))
+            return cache[key][1].gemm(at, out=out, out_dtype=out_dtype, stream=stream)
         ct = self._out(m, out, out_dtype)
         _lib.call("tw_gemm_tew", self._h, at.data_ptr(), m, lda, csc.col_ptr.data_ptr(), csc.row_idx.data_ptr(),
                   csc.values.data_ptr(), csc.nnz, ct.data_ptr(), ct.stride(0), _code(out_dtype), _stream_ptr(stream))
@@ -276,12 +295,56 @@ class DeviceCsc:
         s = as_csc(s)
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.rows, self.cols, self.nnz = s.rows, s.cols, s.nnz
+        self.host = s  # the host matrix (gemm_tew's merged plan is built from it)
         self.col_ptr = torch.from_numpy(np.asarray(s.col_ptr, np.int64).astype(np.int32)).to(dev)
         self.row_idx = torch.from_numpy(np.asarray(s.row_idx, np.int64).astype(np.int32).reshape(-1)).to(dev)
         self.values = torch.from_numpy(np.array(s.values, np.float32).reshape(-1)).to(dev)
         if self.nnz == 0:  # keep valid pointers
             self.row_idx = torch.zeros(1, dtype=torch.int32, device=dev)
             self.values = torch.zeros(1, dtype=torch.float32, device=dev)
+
+
+def tew_merged_tileset(tiles: CompactTileSet, ew: CscMatrix) -> CompactTileSet:
+    """The TEW layer (TW tiles + element-wise overlay, engine.py:184-198) as
+    one tile set for the TW kernel.  Tile t keeps rows kept_t ∪ {overlay rows
+    of its columns}, with weights expand(tiles) + S on them (TEW overlays
+    restore pruned elements, pruning.py:527-561, so the sum only fills
+    zeros); the overlay entries of pruned columns are grouped, ascending, into
+    extra tiles of at most G columns.  C = A · (expand(tiles) + S) = tw + extra
+    up to fp32 summation order."""
+    ew = as_csc(ew)
+    k, n, g = tiles.k, tiles.n, tiles.g
+    if (ew.rows, ew.cols) != (k, n):
+        raise DimensionError(f"overlay is {ew.rows}x{ew.cols}, pattern is {k}x{n}")
+    dense = np.array(tiles.expand().array(), dtype=np.float32, copy=True)
+    cp = np.asarray(ew.col_ptr, np.int64)
+    ri = np.asarray(ew.row_idx, np.int64).reshape(-1)
+    va = np.asarray(ew.values, np.float32).reshape(-1)
+    col_of = np.repeat(np.arange(n, dtype=np.int64), np.diff(cp))
+    np.add.at(dense, (ri, col_of), va)
+    tile_of = np.full(n, -1, np.int64)
+    keeps = []
+    for i, t in enumerate(tiles.tiles):
+        tile_of[np.asarray(t.col_ids, np.int64)] = i
+        keeps.append(unpack_mask_words(t.row_mask_words, k).astype(bool))
+    keeps = np.array(keeps, dtype=bool).reshape(len(tiles.tiles), k)
+    sel = tile_of[col_of] >= 0
+    keeps[tile_of[col_of[sel]], ri[sel]] = True
+    groups = [(np.asarray(t.col_ids, np.int32), keeps[i]) for i, t in enumerate(tiles.tiles)]
+    extra_cols = np.unique(col_of[~sel]).astype(np.int32)
+    for j in range(0, extra_cols.size, g):
+        cols = extra_cols[j: j + g]
+        keep = np.zeros(k, bool)
+        keep[ri[~sel][np.isin(col_of[~sel], cols)]] = True
+        groups.append((cols, keep))
+    out = []
+    for cols, keep in groups:
+        rows = np.flatnonzero(keep)
+        sub = dense[np.ix_(rows, cols.astype(np.int64))]
+        out.append(CompactTile(sub_matrix=DenseMatrix(rows.size, cols.size, Layout.COL_MAJOR,
+                                                      np.ascontiguousarray(sub.T).reshape(-1)),
+                               row_mask_words=pack_mask_words(keep), col_ids=cols))
+    return CompactTileSet(k, n, g, tuple(out))
 
 
 def spmm_csc_device(at, csc: DeviceCsc, out=None, out_dtype=None, accumulate=False, stream=None):

@@ -18,10 +18,13 @@ cp, ri, va = orc.tew_overlay_magnitude(w, p, 0.015)
 csc = tw.DeviceCsc(tw.CscMatrix(k, n, cp, ri, va))
 at = torch.randn((k, m), device="cuda").to(torch.bfloat16)
 out = torch.empty((n, m), device="cuda")
+out16 = torch.empty((n, m), device="cuda", dtype=torch.float16)
 for name, fn in [("spmm overwrite", lambda i: tw.spmm_csc_device(at, csc, out=out)),
                  ("spmm accumulate", lambda i: tw.spmm_csc_device(at, csc, out=out, accumulate=True)),
                  ("tw overwrite", lambda i: plan.gemm(at, out=out)),
                  ("tw accumulate", lambda i: plan.gemm(at, out=out, accumulate=True)),
-                 ("gemm_tew", lambda i: plan.gemm_tew(at, csc, out=out))]:
-    print(f"{name:18s} {timed(fn, 20):8.1f} us", flush=True)
+                 ("gemm_tew (TW + SpMM)", lambda i: plan.gemm_tew(at, csc, out=out, merged=False)),
+                 ("gemm_tew (merged plan)", lambda i: plan.gemm_tew(at, csc, out=out)),
+                 ("gemm_tew merged fp16", lambda i: plan.gemm_tew(at, csc, out=out16, out_dtype=torch.float16))]:
+    print(f"{name:24s} {timed(fn, 20):8.1f} us", flush=True)
 print("nnz", csc.nnz)
