@@ -212,3 +212,26 @@ def test_no_cpu_fallback_without_gpu():
     ts = tw.compact(tw.DenseMatrix.from_array(c["w"]), to_tw_pattern(c["pattern"]))
     with pytest.raises(Exception):
         tw.gemm_tw(tw.DenseMatrix.from_array(c["a"]), ts)
+
+
+@pytest.mark.parametrize("seed,s,delta", [(1, 0.765, 0.015), (2, 0.5, 0.05), (3, 0.9, 0.002)])
+def test_tew_merged_tileset_is_tw_plus_overlay(seed, s, delta):
+    """gemm_tew's merged plan: expand(merged) == expand(tiles) + S exactly,
+    tiles stay disjoint and <= G wide, and it packs."""
+    from paper_2008_13006_b200.engine import tew_merged_tileset
+    k, n, g = 200, 700, 128
+    _, w, p = orc.bench_inputs(8, k, n, g, s, seed=seed)
+    cp, ri, va = orc.tew_overlay_magnitude(w, p, delta)
+    ts = tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p))
+    merged = tew_merged_tileset(ts, tw.CscMatrix(k, n, cp, ri, va))
+    dense_s = np.zeros((k, n), np.float32)
+    dense_s[ri, np.repeat(np.arange(n), np.diff(cp))] = va
+    assert np.array_equal(merged.expand().array(), ts.expand().array() + dense_s)
+    cols = np.concatenate([t.col_ids for t in merged.tiles])
+    assert np.unique(cols).size == cols.size and max(t.col_ids.size for t in merged.tiles) <= g
+    plan = tw.PackedPlan(merged)
+    assert plan.info["kept_elems"] >= ts_kept(ts)
+
+
+def ts_kept(ts):
+    return sum(t.sub_matrix.rows * t.sub_matrix.cols for t in ts.tiles)
