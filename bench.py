@@ -2,6 +2,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--out-dtype fp16|fp32|bf16] [--workload C2a|C2b|C1|C5_75|C4]
+(C4 = TEW: the TW layer plus a 1.5% element-wise overlay, gemm_tew)
 
 One step = one pass of the hot path over one batch: gemm_tw of the BERT-base
 FC1 layer (M=4096 tokens, K=768, N=3072, G=128, 75% TW sparsity, pattern
@@ -49,7 +50,10 @@ WORKLOADS = {
     "C2b": (4096, 768, 768, 128, 0.75, "BERT-base attn-out M=4096 K=768 N=768, G=128, 75% TW"),
     "C1": (1024, 1024, 1024, 128, 0.50, "M=N=K=1024, G=128, 50% TW"),
     "C5_75": (16384, 1024, 4096, 128, 0.75, "BERT-large FC1 M=16384 K=1024 N=4096, G=128, 75% TW"),
+    "C4": (4096, 768, 3072, 128, 0.765, "BERT-base FC1 M=4096 K=768 N=3072, TEW: 76.5% TW + 1.5% element overlay"),
 }
+# TEW workloads: overlay fraction delta (tew_overlay_magnitude, test_engine.py:216-230 recipe)
+TEW_DELTA = {"C4": 0.015}
 L2_BYTES = 126 * 2**20
 
 
@@ -179,18 +183,25 @@ def read_traffic(workload: str, out_dtype: str):
 
 
 # ---------------------------------------------------------------- CPU arm
-def cpu_reference_time(orc, a, w, p, m_sample: int, threads: int, repeats: int):
+def cpu_reference_time(orc, a, w, p, m_sample: int, threads: int, repeats: int, overlay=None):
     """Times the reference's CPU algorithm (oracle C port of gemm_tw,
-    engine.py:126-164 / _kernels.py:13-27) on an M-row sample."""
+    engine.py:126-164 / _kernels.py:13-27, or gemm_tew with an overlay) on an
+    M-row sample."""
     k, n = p[0], p[1]
     packed = orc.PackedTiles(orc.compact(w, p), k, n)
     at = np.ascontiguousarray(a[:m_sample].T)
     out = np.empty((n, m_sample), np.float32)
-    orc.gemm_tw_ct(at, packed, threads=threads, out=out)  # warm-up (time_median semantics)
+
+    def f():
+        if overlay is None:
+            orc.gemm_tw_ct(at, packed, threads=threads, out=out)
+        else:
+            orc.gemm_tew_ct(at, packed, *overlay, threads=threads)
+    f()  # warm-up (time_median semantics)
     times = []
     for _ in range(repeats):
         t0 = time.perf_counter()
-        orc.gemm_tw_ct(at, packed, threads=threads, out=out)
+        f()
         times.append(time.perf_counter() - t0)
     return statistics.median(times)
 
@@ -226,18 +237,27 @@ def run_reference(args):
     dense_flops = 2 * m * k * n
     tilewise = load_reference()
     total_steps = args.steps + args.warmup
+    delta = TEW_DELTA.get(args.workload)
+    overlay = orc.tew_overlay_magnitude(w, p, delta) if delta else None
     if tilewise is not None:
         threads = os.cpu_count() or 1
         pat = tilewise.TilePattern(k, n, g, tuple(tilewise.Tile(c, keep) for c, keep in p[3]))
         tiles = tilewise.compact(tilewise.DenseMatrix.from_array(w), pat)
+        ew = None
+        if overlay is not None:
+            cp, ri, va = overlay
+            ew = tilewise.CscMatrix(k, n, np.asarray(cp, np.uint32), np.asarray(ri, np.uint32),
+                                    np.asarray(va, np.float32))
 
         def run_m(ms):
             a_dm = tilewise.DenseMatrix.from_array(np.ascontiguousarray(a[:ms]))
             def f():
+                if ew is not None:
+                    return tilewise.gemm_tew(a_dm, tiles, ew, workers=threads)
                 return tilewise.gemm_tw(a_dm, tiles, workers=threads)
             return f
-        kind, impl_note = "reference", ("tilewise.gemm_tw (the unmodified reference, numba, installed in "
-                                        "baseline/_ref) with workers=os.cpu_count()")
+        kind, impl_note = "reference", (f"tilewise.{'gemm_tew' if ew is not None else 'gemm_tw'} (the unmodified "
+                                        "reference, numba, installed in baseline/_ref) with workers=os.cpu_count()")
     else:
         threads = orc.max_threads()
         packed = orc.PackedTiles(orc.compact(w, p), k, n)
@@ -246,6 +266,8 @@ def run_reference(args):
             at = np.ascontiguousarray(a[:ms].T)
             out = np.empty((n, ms), np.float32)
             def f():
+                if overlay is not None:
+                    return orc.gemm_tew_ct(at, packed, *overlay, threads=threads)
                 return orc.gemm_tw_ct(at, packed, threads=threads, out=out)
             return f
         kind, impl_note = "port", "oracle/tw_oracle.c, bit-exact C port of the reference's gemm_tw (baseline/_ref absent)"
@@ -327,6 +349,20 @@ def run_ours(args):
     info = plan.info
     dense_flops = 2 * m * k * n_layer
     kept_flops = plan.kept_flops(m)
+    # TEW workloads (C4): the element-wise overlay of tew_overlay_magnitude
+    delta = TEW_DELTA.get(args.workload)
+    overlay = orc.tew_overlay_magnitude(w, p, delta) if delta else None
+    csc_host = dcsc = None
+    if overlay is not None:
+        csc_host = tw.CscMatrix(k, n_total, *overlay)
+        dcsc = tw.DeviceCsc(csc_host, dev)
+        ocols = np.repeat(np.arange(n_total), np.diff(overlay[0]))
+        kept_flops += 2 * m * int(np.count_nonzero((ocols >= col_range[0]) & (ocols < col_range[1])))
+
+    def run(pl, at_, out=None, dt=None, **kw):
+        if dcsc is not None:
+            return pl.gemm_tew(at_, dcsc, out=out, out_dtype=dt)
+        return pl.gemm(at_, out=out, out_dtype=dt, **kw)
 
     # rotating buffer sets so consecutive steps never hit in L2
     at0 = tw.prep_activations(torch.from_numpy(a).to(dev), tw.Layout.ROW_MAJOR, torch.bfloat16)
@@ -339,19 +375,24 @@ def run_ours(args):
     # parity gate (untimed): GPU result (timed output dtype, and fp32) vs the
     # CPU oracle on this rank's slice
     sub = orc.compact(w, p)
-    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(sub, k, n_total),
-                          threads=orc.max_threads())[col_range[0]:col_range[1]]
+    if overlay is None:
+        want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(sub, k, n_total),
+                              threads=orc.max_threads())[col_range[0]:col_range[1]]
+    else:
+        want = orc.gemm_tew_ct(np.ascontiguousarray(a.T), orc.PackedTiles(sub, k, n_total), *overlay,
+                               threads=orc.max_threads())[col_range[0]:col_range[1]]
     prc = orc.pruned_columns(p)
     prc = prc[(prc >= col_range[0]) & (prc < col_range[1])] - col_range[0]
-    ct = plan.gemm(at0, out_dtype=out_dt).float().cpu().numpy()
+    ct = run(plan, at0, dt=out_dt).float().cpu().numpy()
     parity = orc.rel_l2(ct, want)
-    zeros_ok = bool(np.all(ct[prc] == 0))
-    parity_fp32 = orc.rel_l2(plan.gemm(at0, out_dtype=torch.float32).cpu().numpy(), want)
+    # TEW overlays restore elements inside pruned columns: no exact-zero rows
+    zeros_ok = bool(np.all(ct[prc] == 0)) if overlay is None else None
+    parity_fp32 = orc.rel_l2(run(plan, at0, dt=torch.float32).cpu().numpy(), want)
     del ct, want
 
     def step(i):
         j = i % n_sets
-        plans[j].gemm(ats[j], out=outs[j], out_dtype=out_dt)
+        run(plans[j], ats[j], out=outs[j], dt=out_dt)
 
     def barrier():
         if pg is not None:
@@ -369,7 +410,7 @@ def run_ours(args):
     value = world * dense_flops / (ms_all * 1e-3) / 1e12
 
     # ---- dominant kernel roofline: the TW kernel is the only launch per step
-    bytes_alg = algorithmic_bytes(info, m, out_bytes)
+    bytes_alg = algorithmic_bytes(info, m, out_bytes) + (12 * csc_host.nnz if csc_host is not None else 0)
     achieved = bytes_alg / (ms * 1e-3) / 1e9
     traffic = read_traffic(args.workload, args.out_dtype)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -388,7 +429,7 @@ def run_ours(args):
             if dt == out_dt:
                 continue
             vo = [torch.empty((n_layer, m), dtype=dt, device=dev) for _ in range(n_sets)]
-            vms = time_device(torch, lambda i: plans[i % n_sets].gemm(ats[i % n_sets], out=vo[i % n_sets], out_dtype=dt),
+            vms = time_device(torch, lambda i: run(plans[i % n_sets], ats[i % n_sets], out=vo[i % n_sets], dt=dt),
                               args.steps, max(args.warmup, n_sets))
             b = algorithmic_bytes(info, m, ob)
             variants[name] = {"ms_per_step": vms, "tflops_dense_equiv": dense_flops / (vms * 1e-3) / 1e12,
@@ -397,19 +438,28 @@ def run_ours(args):
         # ---- resident output (write_pruned=False): the pruned rows of a
         # reused C^T buffer already hold 0, so only kept rows are written.
         # Reported, not the headline (the reference writes every column).
-        vo = [torch.empty((n_layer, m), dtype=out_dt, device=dev) for _ in range(n_sets)]
-        for j in range(n_sets):
-            plans[j].gemm(ats[j], out=vo[j], out_dtype=out_dt)
-        vms = time_device(torch, lambda i: plans[i % n_sets].gemm(ats[i % n_sets], out=vo[i % n_sets], out_dtype=out_dt,
-                                                                  write_pruned=False),
-                          args.steps, max(args.warmup, n_sets))
-        kept_rows = n_layer - len(prc)
-        b = algorithmic_bytes(info, m, out_bytes) - len(prc) * m * out_bytes
-        variants[f"{args.out_dtype}_out_resident"] = {
-            "ms_per_step": vms, "tflops_dense_equiv": dense_flops / (vms * 1e-3) / 1e12,
-            "hbm_gbs": b / (vms * 1e-3) / 1e9, "hbm_frac": b / (vms * 1e-3) / 1e9 / hbm_peak,
-            "rows_written": kept_rows}
-        del vo
+        if overlay is None:  # (TEW overlays write pruned columns too)
+            vo = [torch.empty((n_layer, m), dtype=out_dt, device=dev) for _ in range(n_sets)]
+            for j in range(n_sets):
+                plans[j].gemm(ats[j], out=vo[j], out_dtype=out_dt)
+            vms = time_device(torch, lambda i: plans[i % n_sets].gemm(ats[i % n_sets], out=vo[i % n_sets],
+                                                                      out_dtype=out_dt, write_pruned=False),
+                              args.steps, max(args.warmup, n_sets))
+            kept_rows = n_layer - len(prc)
+            b = algorithmic_bytes(info, m, out_bytes) - len(prc) * m * out_bytes
+            variants[f"{args.out_dtype}_out_resident"] = {
+                "ms_per_step": vms, "tflops_dense_equiv": dense_flops / (vms * 1e-3) / 1e12,
+                "hbm_gbs": b / (vms * 1e-3) / 1e9, "hbm_frac": b / (vms * 1e-3) / 1e9 / hbm_peak,
+                "rows_written": kept_rows}
+            del vo
+        else:  # the reference's composition (TW-GEMM, then the SpMM accumulated)
+            vo = [torch.empty((n_layer, m), dtype=out_dt, device=dev) for _ in range(n_sets)]
+            vms = time_device(torch, lambda i: plans[i % n_sets].gemm_tew(ats[i % n_sets], dcsc, out=vo[i % n_sets],
+                                                                          out_dtype=out_dt, merged=False),
+                              args.steps, max(args.warmup, n_sets))
+            variants[f"{args.out_dtype}_out_tw_plus_spmm"] = {
+                "ms_per_step": vms, "tflops_dense_equiv": dense_flops / (vms * 1e-3) / 1e12}
+            del vo
         # ---- dense cuBLAS bf16 baseline at the same shape (rotating buffers)
         a_bf = torch.from_numpy(a).to(dev, torch.bfloat16)
         w_bf = torch.from_numpy(w[:, col_range[0]:col_range[1]].copy()).to(dev, torch.bfloat16)
@@ -436,24 +486,29 @@ def run_ours(args):
         c_pin = _t.empty(m * n_total, dtype=_t.float32, pin_memory=True).numpy()
         e2e_ts = ts if world == 1 else None
         if e2e_ts is not None:
+            def e2e_call():
+                if csc_host is not None:
+                    return tw.gemm_tew(a_host, e2e_ts, csc_host, out=c_pin)
+                return tw.gemm_tw(a_host, e2e_ts, out=c_pin)
             for _ in range(max(2, args.warmup)):
-                tw.gemm_tw(a_host, e2e_ts, out=c_pin)
+                e2e_call()
             e_steps = max(3, min(args.steps, 50))
             t0 = time.perf_counter()
             for _ in range(e_steps):
-                r = tw.gemm_tw(a_host, e2e_ts, out=c_pin)
+                r = e2e_call()
             e2e_s = (time.perf_counter() - t0) / e_steps
             assert r.shape == (m, n_total)
             result["e2e"] = {"value": dense_flops / e2e_s / 1e12, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
                              "h2d_bytes_per_step": 4 * m * k, "d2h_bytes_per_step": 4 * m * n_total,
-                             "api": "paper_2008_13006_b200.gemm_tw(DenseMatrix fp32 host, CompactTileSet) -> "
-                                    "COL_MAJOR DenseMatrix (pinned host buffers)"}
+                             "api": (f"paper_2008_13006_b200.{'gemm_tew' if csc_host is not None else 'gemm_tw'}"
+                                     "(DenseMatrix fp32 host, CompactTileSet[, CscMatrix]) -> "
+                                     "COL_MAJOR DenseMatrix (pinned host buffers)")}
 
         # ---- CPU baseline: reference algorithm (oracle C port) on host cores
         if world == 1 and not args.no_cpu:
             threads = orc.max_threads()
             m_s = min(m, args.cpu_sample_m)
-            t_cpu = cpu_reference_time(orc, a, w, p, m_s, threads, repeats=3) * m / m_s
+            t_cpu = cpu_reference_time(orc, a, w, p, m_s, threads, repeats=3, overlay=overlay) * m / m_s
             result["cpu_baseline"] = {"value": dense_flops / t_cpu / 1e12, "unit": UNIT, "cores": threads,
                                       "kind": "port",
                                       "sample": f"gemm_tw on {m_s} of {m} token rows, median of 3 after 1 warm-up, "

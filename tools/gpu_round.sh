@@ -8,7 +8,7 @@ python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-for wl in C2b C1 C5_75; do timeout 600 python bench.py --workload $wl --no-cpu > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err; done
+for wl in C2b C1 C5_75 C4; do timeout 600 python bench.py --workload $wl --no-cpu > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err; done
 timeout 600 python bench.py --out-dtype fp32 --no-cpu > gpurun_out/bench_fp32.json 2> gpurun_out/bench_fp32.err
 TW_B200_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_2rank_gloo.json 2> gpurun_out/bench_2rank_gloo.err
 for wl in C2a C5_75 C2b C1; do timeout 300 python tools/ablate.py --workload $wl --debug 0 3 7 4 64; done > gpurun_out/ablate.log 2>&1
