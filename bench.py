@@ -51,6 +51,8 @@ WORKLOADS = {
     "C1": (1024, 1024, 1024, 128, 0.50, "M=N=K=1024, G=128, 50% TW"),
     "C5_75": (16384, 1024, 4096, 128, 0.75, "BERT-large FC1 M=16384 K=1024 N=4096, G=128, 75% TW"),
     "C4": (4096, 768, 3072, 128, 0.765, "BERT-base FC1 M=4096 K=768 N=3072, TEW: 76.5% TW + 1.5% element overlay"),
+    "C5_50": (16384, 1024, 4096, 128, 0.50, "BERT-large FC1 M=16384 K=1024 N=4096, G=128, 50% TW"),
+    "C5_0": (16384, 1024, 4096, 128, 0.0, "BERT-large FC1 M=16384 K=1024 N=4096, G=128, dense pattern"),
 }
 # TEW workloads: overlay fraction delta (tew_overlay_magnitude, test_engine.py:216-230 recipe)
 TEW_DELTA = {"C4": 0.015}
