@@ -243,6 +243,16 @@ int tw_gemm_traced(const tw_plan *plan, const void *at, int64_t m, int64_t lda, 
 int tw_copy_2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width_bytes, int64_t height,
                int kind, void *stream);
 
+/* Pruning unit scores on the GPU (pruning.py:293, :316-318; SURVEY §8(f)
+ * row 4).  scores: device K x N float64, row-major (ScoreMap.scores).
+ * tw_prune_col_means: out[j] = mean over rows of column j (s.mean(axis=0)).
+ * tw_prune_row_means: for tile t with columns cols[off[t] .. off[t+1]),
+ * out[t*K + r] = mean of s[r, cols_t] (s[:, cols].mean(axis=1)).  Both sum
+ * sequentially in numpy's order, so the means are bit-identical. */
+int tw_prune_col_means(const double *scores, int64_t k, int64_t n, double *out, void *stream);
+int tw_prune_row_means(const double *scores, int64_t k, int64_t n, const int32_t *cols, const int64_t *off,
+                       int64_t n_tiles, double *out, void *stream);
+
 /* Number of SMs used by the persistent grid on the current device. */
 int tw_device_sm_count(int *sms);
 

@@ -37,6 +37,7 @@ from .pattern import (
 )
 from .sharded import ShardedTwPlan, all_gather_rows, shard_ranges
 from .layers import TwMlp, engine_logits
+from .pruning import prune_stage
 from .formats import (plan_from_files, read_csc, read_matrix, read_model, read_pattern, write_csc, write_matrix,
                       write_pattern)
 from .engine import (

@@ -59,6 +59,8 @@ SIGNATURES = {
     "tw_ipc_free": (_i32, [_p]),
     "tw_ipc_open": (_i32, [_p, _p]),
     "tw_ipc_close": (_i32, [_p]),
+    "tw_prune_col_means": (_i32, [_p, _i64, _i64, _p, _p]),
+    "tw_prune_row_means": (_i32, [_p, _i64, _i64, _p, _p, _i64, _p, _p]),
     "tw_gemm_exact": (_i32, [_p, _p, _i64, _i64, _p, _i64, _p]),
     "tw_prep_activations": (_i32, [_p, _i64, _i64, _i32, _p, _i64, _i32, _p]),
     "tw_spmm_csc": (_i32, [_p, _i32, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _i32, _i32, _p]),

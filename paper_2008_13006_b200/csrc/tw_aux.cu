@@ -501,6 +501,43 @@ cudaError_t spmm_at(const void *at, int64_t m, int64_t k, int64_t lda, int64_t c
 
 }  // namespace
 
+// ------------------------------------------------------- pruning scores
+// prune_stage's unit scores (pruning.py:293 and :316-318), the step before
+// the TW path.  numpy reduces axis 0 of the C-contiguous
+// K x N float64 score map row after row, and the K x n_t fancy-indexed copy
+// s[:, cols] along axis 1 column after column -- both plain sequential
+// float64 sums (pinned by tests/golden/golden_prune.npz) -- then divides by
+// the count.  One thread per output keeps exactly that order.
+__global__ void prune_col_mean_kernel(const double *__restrict__ s, int64_t k, int64_t n, double *__restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double acc = 0.0;
+  for (int64_t r = 0; r < k; ++r) acc += s[r * n + j];
+  out[j] = acc / (double)k;
+}
+
+__global__ void prune_row_mean_kernel(const double *__restrict__ s, int64_t k, int64_t n,
+                                      const int32_t *__restrict__ cols, const int64_t *__restrict__ off,
+                                      int64_t n_tiles, double *__restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_tiles * k) return;
+  const int64_t t = idx / k, r = idx % k;
+  const int64_t c0 = off[t], c1 = off[t + 1];
+  double acc = 0.0;
+  for (int64_t c = c0; c < c1; ++c) acc += s[r * n + cols[c]];
+  out[idx] = acc / (double)(c1 - c0);
+}
+
+cudaError_t launch_prune_means(const double *s, int64_t k, int64_t n, const int32_t *cols, const int64_t *off,
+                               int64_t n_tiles, double *out, cudaStream_t st) {
+  if (cols == nullptr) {
+    prune_col_mean_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, k, n, out);
+  } else {
+    prune_row_mean_kernel<<<(unsigned)((n_tiles * k + 255) / 256), 256, 0, st>>>(s, k, n, cols, off, n_tiles, out);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
                         cudaStream_t s) {
   switch (out_dtype) {

@@ -19,6 +19,8 @@ cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t k, int6
                         int accumulate, cudaStream_t s);
 cudaError_t launch_exact(const tw_plan *p, const float *at, int64_t m, int64_t lda, float *ct, int64_t ldc,
                          cudaStream_t s);
+cudaError_t launch_prune_means(const double *s, int64_t k, int64_t n, const int32_t *cols, const int64_t *off,
+                               int64_t n_tiles, double *out, cudaStream_t st);
 
 
 namespace {
@@ -362,6 +364,30 @@ int tw_gemm_exact(const tw_plan *p, const float *at, int64_t m, int64_t lda, flo
   cudaError_t e = launch_exact(p, at, m, lda, ct, ldc, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tw_gemm_exact launch");
   return TW_OK;
+}
+
+int tw_prune_col_means(const double *scores, int64_t k, int64_t n, double *out, void *stream) {
+  clear_error();
+  if (!scores || !out) return fail(TW_ERR_ARG, "null pointer");
+  if (k < 1 || n < 1) return fail(TW_ERR_DIMENSION, "bad score-map dims");
+  int sms = 0;
+  int rc = require_sm100(&sms);
+  if (rc) return rc;
+  cudaError_t e = launch_prune_means(scores, k, n, nullptr, nullptr, 0, out, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TW_OK : cuda_fail(e, "tw_prune_col_means launch");
+}
+
+int tw_prune_row_means(const double *scores, int64_t k, int64_t n, const int32_t *cols, const int64_t *off,
+                       int64_t n_tiles, double *out, void *stream) {
+  clear_error();
+  if (!scores || !cols || !off || !out) return fail(TW_ERR_ARG, "null pointer");
+  if (k < 1 || n < 1 || n_tiles < 0) return fail(TW_ERR_DIMENSION, "bad score-map dims");
+  if (n_tiles == 0) return TW_OK;
+  int sms = 0;
+  int rc = require_sm100(&sms);
+  if (rc) return rc;
+  cudaError_t e = launch_prune_means(scores, k, n, cols, off, n_tiles, out, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? TW_OK : cuda_fail(e, "tw_prune_row_means launch");
 }
 
 int tw_prep_activations(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
