@@ -179,7 +179,8 @@ class ShardedTwPlan:
         nbytes = max(1, rows * m * esize)
         ptr = ctypes.c_void_p()
         handle = (ctypes.c_char * 64)()
-        _lib.call("tw_ipc_alloc", nbytes, ctypes.byref(ptr), ctypes.cast(handle, ctypes.c_void_p))
+        with torch.cuda.device(self.device):  # allocate / map on the plan's GPU
+            _lib.call("tw_ipc_alloc", nbytes, ctypes.byref(ptr), ctypes.cast(handle, ctypes.c_void_p))
         handles = [None] * self.world
         dist.all_gather_object(handles, bytes(handle), group=self.group)
         ptrs = []
@@ -189,7 +190,8 @@ class ShardedTwPlan:
             else:
                 pp = ctypes.c_void_p()
                 hb = (ctypes.c_char * 64).from_buffer_copy(h)
-                _lib.call("tw_ipc_open", ctypes.cast(hb, ctypes.c_void_p), ctypes.byref(pp))
+                with torch.cuda.device(self.device):
+                    _lib.call("tw_ipc_open", ctypes.cast(hb, ctypes.c_void_p), ctypes.byref(pp))
                 ptrs.append(pp.value)
         full = _device_view(ptr.value, (rows, m), out_dtype, self.device)
         full.zero_()  # rows past N stay zero
