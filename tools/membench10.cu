@@ -90,9 +90,16 @@ void run(const char *name, Geo g, long long *cyc, int sms) {
   cudaMemcpy(kept, hk.data(), hk.size() * 4, cudaMemcpyHostToDevice);
   const int smem = kDepth * (kA + kB) + 1024 + 256;
   cudaFuncSetAttribute(gather<kDepth>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms = 0.f;
   for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0);
     gather<kDepth><<<sms, 128, smem>>>(at, wimg, kept, g, cyc);
+    cudaEventRecord(e1);
     cudaDeviceSynchronize();
+    cudaEventElapsedTime(&ms, e0, e1);
   }
   long long h[256];
   cudaMemcpy(h, cyc, sms * 8, cudaMemcpyDeviceToHost);
@@ -100,8 +107,8 @@ void run(const char *name, Geo g, long long *cyc, int sms) {
   for (int i = 0; i < sms; ++i) { avg += h[i]; mx = std::max(mx, (double)h[i]); }
   avg /= sms;
   const double bytes = (double)g.units_per_cta * (g.keep / 64) * (kA + kB);
-  printf("depth %d %-40s A+W %6.1f B/clk/SM avg, slowest CTA %6.1f  (%s)\n", kDepth, name, bytes / avg, bytes / mx,
-         cudaGetErrorString(cudaGetLastError()));
+  printf("depth %d %-40s A+W %6.1f B/clk/SM avg, slowest CTA %6.1f, launch %7.2f us (%s)\n", kDepth, name, bytes / avg,
+         bytes / mx, ms * 1e3, cudaGetErrorString(cudaGetLastError()));
   cudaFree(at);
   cudaFree(wimg);
   cudaFree(kept);
@@ -112,14 +119,9 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   long long *cyc;
   cudaMalloc(&cyc, 256 * 8);
-  for (int rep = 0; rep < 1; ++rep) {
-    run<3>("C2a 768x4096, 12 tiles, 8 units/CTA", Geo{768, 4096, 4096, 384, 12, 8}, cyc, sms);
-    run<4>("C2a 768x4096, 12 tiles, 8 units/CTA", Geo{768, 4096, 4096, 384, 12, 8}, cyc, sms);
-    run<3>("C2a, 2 units/CTA", Geo{768, 4096, 4096, 384, 12, 2}, cyc, sms);
-    run<4>("C2a, 2 units/CTA", Geo{768, 4096, 4096, 384, 12, 2}, cyc, sms);
-    run<3>("C5 1024x16384, 16 tiles, 7 units/CTA", Geo{1024, 16384, 16384, 512, 16, 7}, cyc, sms);
-    run<4>("C5 1024x16384, 16 tiles, 7 units/CTA", Geo{1024, 16384, 16384, 512, 16, 7}, cyc, sms);
-  }
+  run<3>("C2a 768x4096, 12 tiles, 2 units/CTA", Geo{768, 4096, 4096, 384, 12, 2}, cyc, sms);
+  run<3>("C5 1024x16384, 16 tiles, 7 units/CTA", Geo{1024, 16384, 16384, 512, 16, 7}, cyc, sms);
+  run<3>("C5 dense 1024x16384, 32 tiles, 14 units/CTA", Geo{1024, 16384, 16384, 1024, 32, 14}, cyc, sms);
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
