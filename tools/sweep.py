@@ -11,7 +11,7 @@ Rows:
   C5   BERT-large FC1 16384x1024x4096, sparsity 0 / .1 / .25 / .5 / .75 / .9
 
 Per row: TW kernel time (CUDA events, mean of `reps` launches over rotating
-output buffers when the output is smaller than 2x L2), fp32 and fp16 output;
+output buffers when the output is smaller than 2x L2; calls graph-captured and replayed), fp32 and fp16 output;
 dense cuBLAS bf16 (torch.mm, bf16 out) at the same shape; dense-equivalent
 and kept TFLOPS; algorithmic HBM bytes and GB/s; speedup vs cuBLAS.  Parity:
 rel-L2 of the fp32 output against the CPU oracle on a token slice (the first
@@ -62,12 +62,20 @@ def rows(quick: bool):
 
 
 def timed(fn, reps):
-    fn(0)
+    """us per call: `reps` calls captured into one CUDA graph and replayed
+    (kernel time without per-call host launch overhead, as in bench.py)."""
+    for i in range(2):
+        fn(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            fn(i)
+    g.replay()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for i in range(reps):
-        fn(i)
+    g.replay()
     b.record()
     torch.cuda.synchronize()
     return a.elapsed_time(b) / reps * 1e3  # us
