@@ -499,6 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 #pragma unroll
       for (int r = 1; r < kRowsPerWarp; ++r) min_row = min(min_row, rows[r]);
       const bool fast = min_row >= 0 && rec.y + nq * 64 <= args.M && !(args.debug & 256);
+      // (tracing) the row indices and the record are in registers here
+      const long long c2b = traced ? clock64() + (min_row & 0) : 0;
       // Units narrower than 256 tokens: R = 4 / nq rows per instruction
       // (8 * nq lanes per row) so no lane idles -- fewer LDGSTS per stage.
       auto gather_rows = [&](auto rr) {
@@ -549,8 +551,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (threadIdx.x == 0) trace_stage(args, i, 0);
       if (threadIdx.x == 0 && args.trace != nullptr && i < 32) {
         const long long c3 = clock64();
+        // 4 x 16 bits: wait_empty, wait_idx, index smem loads, issue
         args.trace[(int64_t)gridDim.x * 64 + ((int64_t)blockIdx.x * 32 + i) * 4 + 3] =
-            (min(c1 - c0, 0xfffffLL) << 40) | (min(c2 - c1, 0xfffffLL) << 20) | min(c3 - c2, 0xfffffLL);
+            (min(c1 - c0, 0xffffLL) << 48) | (min(c2 - c1, 0xffffLL) << 32) | (min(c2b - c2, 0xffffLL) << 16) |
+            min(c3 - c2b, 0xffffLL);
       }
       if (threadIdx.x == 0 && (rec.w & (1 << 17))) trace_evt(args, rec.w & 0xffff, 1);
       if (++stage == C::kStages) { stage = 0; phase ^= 1; }

@@ -104,12 +104,13 @@ def main():
         print(f"{si:5d} {np.nanmedian(srel[:, si, 0]):9.2f} {np.nanmedian(srel[:, si, 1]):9.2f} "
               f"{np.nanmedian(srel[:, si, 2]):9.2f}     [{c0[0]:7.2f} {c0[1]:7.2f} {c0[2]:7.2f}]")
     raw3 = full[sms.value * 64: sms.value * 192].reshape(sms.value, 32, 4)[:, :, 3].astype(np.int64)
-    print("producer cycles per stage (median over CTAs): wait_empty wait_idx issue")
+    print("producer cycles per stage (median over CTAs): wait_empty wait_idx index_lds issue")
     for si in range(12):
         v = raw3[:, si]
         v = v[v > 0]
         if v.size:
-            print(f"  stage {si:2d}: {np.median(v >> 40):7.0f} {np.median((v >> 20) & 0xfffff):7.0f} {np.median(v & 0xfffff):7.0f}")
+            print(f"  stage {si:2d}: {np.median(v >> 48):7.0f} {np.median((v >> 32) & 0xffff):7.0f} "
+                  f"{np.median((v >> 16) & 0xffff):7.0f} {np.median(v & 0xffff):7.0f}")
     base = np.where(ep[:, :1] > 0, ep[:, :1], np.nan)
     erel = np.where(ep > 0, ep - base, np.nan)  # SM cycles since chunk 0's TMEM load completed
     print("epilogue chunk c of unit 0 (median over CTAs, SM cycles from chunk-0 ld): ld_done sts_done synced stored")
