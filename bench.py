@@ -53,6 +53,14 @@ WORKLOADS = {
     "C4": (4096, 768, 3072, 128, 0.765, "BERT-base FC1 M=4096 K=768 N=3072, TEW: 76.5% TW + 1.5% element overlay"),
     "C5_50": (16384, 1024, 4096, 128, 0.50, "BERT-large FC1 M=16384 K=1024 N=4096, G=128, 50% TW"),
     "C5_0": (16384, 1024, 4096, 128, 0.0, "BERT-large FC1 M=16384 K=1024 N=4096, G=128, dense pattern"),
+    "C5_90": (16384, 1024, 4096, 128, 0.90, "BERT-large FC1 M=16384 K=1024 N=4096, G=128, 90% TW"),
+    # NMT: assumed shape (PAPER.md:626-627 gives none): the gate GEMM of a
+    # 512-unit LSTM layer, [x_t; h_{t-1}] (K=1024) -> 4 gates (N=2048), 4096 tokens
+    "NMT": (4096, 1024, 2048, 128, 0.75, "NMT LSTM gate GEMM M=4096 K=1024 N=2048 (assumed), G=128, 75% TW"),
+    # VGG-16 conv layers as im2col GEMMs at batch 64 (BASELINE config 3): M = 64*H*W
+    "VGG_conv1_2": (3211264, 576, 64, 128, 0.75, "VGG-16 conv1_2 im2col b64: M=3211264 K=576 N=64, 75% TW"),
+    "VGG_conv3_2": (200704, 2304, 256, 128, 0.75, "VGG-16 conv3_2 im2col b64: M=200704 K=2304 N=256, 75% TW"),
+    "VGG_conv4_2": (50176, 4608, 512, 128, 0.50, "VGG-16 conv4_2 im2col b64: M=50176 K=4608 N=512, 50% TW"),
 }
 # TEW workloads: overlay fraction delta (tew_overlay_magnitude, test_engine.py:216-230 recipe)
 TEW_DELTA = {"C4": 0.015}

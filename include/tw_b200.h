@@ -105,7 +105,23 @@ typedef struct tw_plan_info {
   int64_t block_n;             /* MMA N tile (128 or 256) */
   int64_t wimg_bytes;          /* packed weight image bytes on device */
   int in_dtype;                /* TW_BF16 or TW_F16 */
+  int flags;                   /* TW_PLAN_* the plan was built with */
+  int64_t a_rows;              /* rows of the A^T operand tw_gemm reads: K, or 2K (TW_PLAN_SPLIT3) */
 } tw_plan_info;
+
+/* Plan flags (tw_plan_create_ex).
+ * TW_PLAN_SPLIT3: fp32-faithful tensor-core mode.  Weights and activations
+ *   are split into bf16 high/low parts, x = hi + lo with hi = rn_bf16(x),
+ *   lo = rn_bf16(x - hi); the plan computes A.W as Ah.Wh + Al.Wh + Ah.Wl (3
+ *   k_i kept rows per tile) from the 2K-row operand [Ah; Al] that
+ *   tw_prep_activations_split writes.  Relative error per product ~2^-17:
+ *   the reference's fp32 acceptance bar (1e-4*K max-abs,
+ *   test_acceptance.py:63-81) on unrounded fp32 inputs.  Needs TW_BF16.
+ * TW_PLAN_F32_WEIGHTS: keep the fp32 weights (the reference's sub_matrix
+ *   values, pattern.py:233) on the device so tw_gemm_exact reproduces
+ *   gemm_tw bit for bit on ANY fp32 weights, not only bf16-representable ones. */
+#define TW_PLAN_SPLIT3 1
+#define TW_PLAN_F32_WEIGHTS 2
 
 /* Build a plan from the reference's compact form (the same arrays as
  * tw_compact's outputs plus the pattern) and upload it to the current
@@ -125,6 +141,11 @@ int tw_plan_build_host(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const i
                        const int32_t *col_ids, const uint32_t *row_mask_words, const float *subs,
                        const int64_t *sub_off, int in_dtype, int64_t col_begin, int64_t col_end,
                        tw_plan **out);
+/* tw_plan_create with TW_PLAN_* flags (0 = tw_plan_create). */
+int tw_plan_create_ex(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,
+                      const int32_t *col_ids, const uint32_t *row_mask_words, const float *subs,
+                      const int64_t *sub_off, int in_dtype, int64_t col_begin, int64_t col_end, int flags,
+                      tw_plan **out);
 int tw_plan_destroy(tw_plan *plan);
 int tw_plan_get_info(const tw_plan *plan, tw_plan_info *info);
 
@@ -200,9 +221,12 @@ int tw_ipc_open(const void *handle, void **ptr);
 int tw_ipc_close(void *ptr);
 
 /* Bit-exact CUDA-core variant of tw_gemm: fp32 multiply then fp32 add, in
- * ascending k per element (exactly mm_accum's rounding sequence); used to
- * prove layouts/indexing independent of tensor-core accumulation order.
- * Same arguments as tw_gemm; activations must be fp32 (in_dtype ignored). */
+ * ascending k per element (exactly mm_accum's rounding sequence,
+ * _kernels.py:13-27).  Weights: the plan's fp32 copy when it was built with
+ * TW_PLAN_F32_WEIGHTS (bit-exact with the reference for any fp32 input --
+ * the drop-in's precision="exact"), else the 16-bit image (bit-exact for
+ * bf16-representable weights, which proves the packed layout).  Same
+ * arguments as tw_gemm; activations are fp32; not for TW_PLAN_SPLIT3 plans. */
 int tw_gemm_exact(const tw_plan *plan, const float *at, int64_t m, int64_t lda, float *ct,
                   int64_t ldc, void *stream);
 
@@ -211,6 +235,11 @@ int tw_gemm_exact(const tw_plan *plan, const float *at, int64_t m, int64_t lda, 
  * at: K x M in out_dtype (TW_BF16 | TW_F16 | TW_F32) with row stride ldat. */
 int tw_prep_activations(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat,
                         int out_dtype, void *stream);
+/* tw_prep_activations for TW_PLAN_SPLIT3 plans: at2 is 2K x M bf16 (row
+ * stride ldat), rows 0..K-1 = rn_bf16(A^T) and rows K..2K-1 =
+ * rn_bf16(A^T - rn_bf16(A^T)) -- the high and low parts. */
+int tw_prep_activations_split(const float *a, int64_t m, int64_t k, int layout, void *at2, int64_t ldat,
+                              void *stream);
 
 /* engine.py:167-181 spmm_csc (+ spmm_accum, _kernels.py:30-41): for each
  * CSC column j, ct[j, :] (+)= sum_p values[p] * at[row_idx[p], :], p in

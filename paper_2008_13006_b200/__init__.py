@@ -37,11 +37,18 @@ from .pattern import (
 )
 from .sharded import ShardedTwPlan, all_gather_rows, shard_ranges
 from .layers import TwMlp, engine_logits
-from .pruning import prune_stage
+from .pruning import ScoreMap, TewConfig, magnitude_scores, prune_stage, tew_overlay
 from .formats import (plan_from_files, read_csc, read_matrix, read_model, read_pattern, write_csc, write_matrix,
                       write_pattern)
 from .engine import (
+    PRECISIONS,
+    BatchGroup,
     DeviceCsc,
+    TileTask,
+    execute_batched,
+    gather_rows,
+    group_by_shape,
+    prep_activations_split,
     FlopReport,
     PackedPlan,
     TwPlan,

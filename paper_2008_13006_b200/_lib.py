@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtw_b200.
 TW_OK, TW_ERR_DIMENSION, TW_ERR_FORMAT = 0, 1, 2
 TW_F32, TW_BF16, TW_F16 = 0, 1, 2
 TW_ROW_MAJOR, TW_COL_MAJOR = 0, 1
+TW_PLAN_SPLIT3, TW_PLAN_F32_WEIGHTS = 1, 2
 
 # every symbol include/tw_b200.h declares: name -> (restype, argtypes)
 _p = ctypes.c_void_p
@@ -31,7 +32,8 @@ class PlanInfo(ctypes.Structure):
                 ("n_tiles", ctypes.c_int64), ("n_live", ctypes.c_int64),
                 ("n_zero_rows", ctypes.c_int64), ("kept_elems", ctypes.c_int64),
                 ("union_k", ctypes.c_int64), ("sum_k", ctypes.c_int64), ("sum_n", ctypes.c_int64),
-                ("block_n", ctypes.c_int64), ("wimg_bytes", ctypes.c_int64), ("in_dtype", ctypes.c_int)]
+                ("block_n", ctypes.c_int64), ("wimg_bytes", ctypes.c_int64), ("in_dtype", ctypes.c_int),
+                ("flags", ctypes.c_int), ("a_rows", ctypes.c_int64)]
 
 
 SIGNATURES = {
@@ -44,6 +46,8 @@ SIGNATURES = {
     "tw_pruned_columns": (_i32, [_i64, _i64, _p, _p, _p, _pi64]),
     "tw_plan_create": (_i32, [_i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _i64, _i64,
                               ctypes.POINTER(ctypes.c_void_p)]),
+    "tw_plan_create_ex": (_i32, [_i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _i64, _i64, _i32,
+                                 ctypes.POINTER(ctypes.c_void_p)]),
     "tw_plan_build_host": (_i32, [_i64, _i64, _i64, _i64, _p, _p, _p, _p, _p, _i32, _i64, _i64,
                                   ctypes.POINTER(ctypes.c_void_p)]),
     "tw_plan_destroy": (_i32, [_p]),
@@ -63,6 +67,7 @@ SIGNATURES = {
     "tw_prune_row_means": (_i32, [_p, _i64, _i64, _p, _p, _i64, _p, _p]),
     "tw_gemm_exact": (_i32, [_p, _p, _i64, _i64, _p, _i64, _p]),
     "tw_prep_activations": (_i32, [_p, _i64, _i64, _i32, _p, _i64, _i32, _p]),
+    "tw_prep_activations_split": (_i32, [_p, _i64, _i64, _i32, _p, _i64, _p]),
     "tw_spmm_csc": (_i32, [_p, _i32, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _i32, _i32, _p]),
     "tw_gemm_tew": (_i32, [_p, _p, _i64, _i64, _p, _p, _p, _i64, _p, _i64, _i32, _p]),
     "tw_device_sm_count": (_i32, [ctypes.POINTER(ctypes.c_int)]),

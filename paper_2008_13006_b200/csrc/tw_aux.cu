@@ -33,32 +33,113 @@ template <>
 __device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
 
 // ---------------------------------------------------------------- prep
-// ROW_MAJOR A (M x K) -> at (K x M): 64x64 tiles through shared memory,
-// coalesced fp32 reads along K and coalesced 16-bit writes along M.
+// A (fp32) -> A^T (K x M) in T, the reference's `at = a.array().T` copy
+// (engine.py:129) with the cast fused.  kSplit (bf16 only): also the low
+// parts, rows K..2K-1 = rn(a - rn(a)) -- the operand of TW_PLAN_SPLIT3.
 template <typename T>
-__global__ void __launch_bounds__(256) prep_transpose_kernel(const float *__restrict__ a, int64_t m, int64_t k,
-                                                             T *__restrict__ at, int64_t ldat) {
-  __shared__ float tile[64][65];
-  const int64_t m0 = (int64_t)blockIdx.y * 64, k0 = (int64_t)blockIdx.x * 64;
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
-  for (int r = ty; r < 64; r += 4) {
-    const int64_t mm = m0 + r, kk = k0 + tx;
-    tile[r][tx] = (mm < m && kk < k) ? __ldg(a + mm * k + kk) : 0.f;
-  }
-  __syncthreads();
-  for (int r = ty; r < 64; r += 4) {
-    const int64_t kk = k0 + r, mm = m0 + tx;
-    if (kk < k && mm < m) at[kk * ldat + mm] = to_t<T>(tile[tx][r]);
+__device__ __forceinline__ void store8(T *dst, const float *v, bool vec) {
+  if (vec) {
+    if constexpr (sizeof(T) == 4) {
+      reinterpret_cast<float4 *>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4 *>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        T lo = to_t<T>(v[2 * i]), hi = to_t<T>(v[2 * i + 1]);
+        w[i] = (uint32_t)*reinterpret_cast<uint16_t *>(&lo) | ((uint32_t)*reinterpret_cast<uint16_t *>(&hi) << 16);
+      }
+      *reinterpret_cast<uint4 *>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[i] = to_t<T>(v[i]);
   }
 }
-// COL_MAJOR A (its buffer is already A^T, K x M with row stride M): cast copy
-template <typename T>
+
+// ROW_MAJOR A (M x K): tiles of 128 tokens x 32 k through shared memory --
+// 16-byte fp32 loads along K, 16-byte 16-bit stores along M (a 256 B run
+// per A^T row per tile), conflict-free shared accesses (row stride 129).
+template <typename T, bool kSplit>
+__global__ void __launch_bounds__(256) prep_transpose_kernel(const float *__restrict__ a, int64_t m, int64_t k,
+                                                             T *__restrict__ at, int64_t ldat) {
+  __shared__ float tile[32][129];
+  const int64_t m0 = (int64_t)blockIdx.x * 128, k0 = (int64_t)blockIdx.y * 32;
+  const bool vin = (k % 4) == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int idx = threadIdx.x + it * 256;
+    const int r = idx >> 3, c = idx & 7;  // token row r, k quad c
+    const int64_t mm = m0 + r, kk = k0 + 4 * c;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (mm < m) {
+      if (vin && kk + 4 <= k) {
+        const float4 q = __ldg(reinterpret_cast<const float4 *>(a + mm * k + kk));
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (kk + i < k) v[i] = __ldg(a + mm * k + kk + i);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tile[4 * c + i][r] = v[i];
+  }
+  __syncthreads();
+  const bool vout = (ldat % 8) == 0 && (reinterpret_cast<uintptr_t>(at) & 15) == 0;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int q = threadIdx.x + it * 256;
+    const int kr = q >> 4, mc = (q & 15) * 8;  // k row, first of 8 tokens
+    const int64_t kk = k0 + kr, mm = m0 + mc;
+    if (kk >= k || mm >= m) continue;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = tile[kr][mc + i];
+    const bool full = mm + 8 <= m;
+    if (full) {
+      store8<T>(at + kk * ldat + mm, v, vout);
+      if constexpr (kSplit) {
+        float lo[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) lo[i] = v[i] - to_f<T>(to_t<T>(v[i]));
+        store8<T>(at + (kk + k) * ldat + mm, lo, vout);
+      }
+    } else {
+      for (int i = 0; i < 8 && mm + i < m; ++i) {
+        at[kk * ldat + mm + i] = to_t<T>(v[i]);
+        if constexpr (kSplit) at[(kk + k) * ldat + mm + i] = to_t<T>(v[i] - to_f<T>(to_t<T>(v[i])));
+      }
+    }
+  }
+}
+// COL_MAJOR A (its buffer is already A^T, K x M with row stride M): cast copy,
+// 8 tokens per thread (two 16-byte loads, one 16-byte store) when aligned
+template <typename T, bool kSplit>
 __global__ void __launch_bounds__(256) prep_cast_kernel(const float *__restrict__ a, int64_t m, int64_t k,
                                                         T *__restrict__ at, int64_t ldat) {
-  const int64_t total = m * k;
+  const bool vec = (m % 8) == 0 && (ldat % 8) == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(at) & 15) == 0;
+  const int64_t per_row = vec ? m / 8 : m;
+  const int64_t total = per_row * k;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t kk = i / m, mm = i - kk * m;
-    at[kk * ldat + mm] = to_t<T>(__ldg(a + i));
+    const int64_t kk = i / per_row, j = i - kk * per_row;
+    if (vec) {
+      const float4 *src = reinterpret_cast<const float4 *>(a + kk * m + 8 * j);
+      const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
+      float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      store8<T>(at + kk * ldat + 8 * j, v, true);
+      if constexpr (kSplit) {
+        float lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) lo[e] = v[e] - to_f<T>(to_t<T>(v[e]));
+        store8<T>(at + (kk + k) * ldat + 8 * j, lo, true);
+      }
+    } else {
+      const float v = __ldg(a + kk * m + j);
+      at[kk * ldat + j] = to_t<T>(v);
+      if constexpr (kSplit) at[(kk + k) * ldat + j] = to_t<T>(v - to_f<T>(to_t<T>(v)));
+    }
   }
 }
 
@@ -373,6 +454,8 @@ __global__ void __launch_bounds__(128) exact_gemm_kernel(const TileMeta *__restr
                                                          const int32_t *__restrict__ kidx,
                                                          const int32_t *__restrict__ colids,
                                                          const uint8_t *__restrict__ wimg, int wbytes, int in_dtype,
+                                                         const float *__restrict__ w32,
+                                                         const int64_t *__restrict__ w32_off,
                                                          const float *__restrict__ at, int64_t m, int64_t lda,
                                                          float *__restrict__ ct, int64_t ldc) {
   const TileMeta t = tiles[blockIdx.y];
@@ -388,7 +471,9 @@ __global__ void __launch_bounds__(128) exact_gemm_kernel(const TileMeta *__restr
     for (int e = threadIdx.x; e < 64 * 16; e += 128) {
       const int r = e >> 4, j = e & 15, n = n0 + j, kk = kb * 64 + r;
       float w = 0.f;
-      if (n < t.n_i && kk < t.k_i) {
+      if (n < t.n_i && kk < t.k_i && w32 != nullptr) {  // TW_PLAN_F32_WEIGHTS: the reference's fp32 values
+        w = __ldg(w32 + __ldg(w32_off + blockIdx.y) + (int64_t)kk * 128 + n);
+      } else if (n < t.n_i && kk < t.k_i) {
         const int c = r >> 3, x = r & 7;
         const uint16_t bits = *reinterpret_cast<const uint16_t *>(
             wimg + t.w_off + (int64_t)kb * wbytes + n * 128 + ((c ^ (n & 7)) * 16) + x * 2);
@@ -424,15 +509,15 @@ __global__ void zero_rows_f32_kernel(const int32_t *__restrict__ rows, int n_row
   }
 }
 
-template <typename T>
+template <typename T, bool kSplit>
 cudaError_t prep_t(const float *a, int64_t m, int64_t k, int layout, T *at, int64_t ldat, cudaStream_t s) {
   if (layout == TW_ROW_MAJOR) {
-    dim3 grid((unsigned)((k + 63) / 64), (unsigned)((m + 63) / 64));
-    prep_transpose_kernel<T><<<grid, 256, 0, s>>>(a, m, k, at, ldat);
+    dim3 grid((unsigned)((m + 127) / 128), (unsigned)((k + 31) / 32));
+    prep_transpose_kernel<T, kSplit><<<grid, 256, 0, s>>>(a, m, k, at, ldat);
   } else {
-    int64_t blocks = (m * k + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    prep_cast_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(a, m, k, at, ldat);
+    int64_t blocks = (m * k / 8 + 255) / 256 + 1;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    prep_cast_kernel<T, kSplit><<<(unsigned)blocks, 256, 0, s>>>(a, m, k, at, ldat);
   }
   return cudaGetLastError();
 }
@@ -541,16 +626,21 @@ cudaError_t launch_prune_means(const double *s, int64_t k, int64_t n, const int3
 cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
                         cudaStream_t s) {
   switch (out_dtype) {
-    case TW_F32: return prep_t<float>(a, m, k, layout, reinterpret_cast<float *>(at), ldat, s);
-    case TW_BF16: return prep_t<__nv_bfloat16>(a, m, k, layout, reinterpret_cast<__nv_bfloat16 *>(at), ldat, s);
-    case TW_F16: return prep_t<__half>(a, m, k, layout, reinterpret_cast<__half *>(at), ldat, s);
+    case TW_F32: return prep_t<float, false>(a, m, k, layout, reinterpret_cast<float *>(at), ldat, s);
+    case TW_BF16: return prep_t<__nv_bfloat16, false>(a, m, k, layout, reinterpret_cast<__nv_bfloat16 *>(at), ldat, s);
+    case TW_F16: return prep_t<__half, false>(a, m, k, layout, reinterpret_cast<__half *>(at), ldat, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_prep_split(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, cudaStream_t s) {
+  return prep_t<__nv_bfloat16, true>(a, m, k, layout, reinterpret_cast<__nv_bfloat16 *>(at), ldat, s);
 }
 
 cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t k, int64_t lda, int64_t col_begin, int64_t n_cols,
                         const int32_t *cp, const int32_t *ri, const float *va, void *ct, int64_t ldc, int out_dtype,
                         int accumulate, cudaStream_t s) {
+  if (m == 0 || n_cols <= 0) return cudaSuccess;  // nothing to write (and no zero-width column groups)
   switch (at_dtype) {
     case TW_F32: return spmm_at<float>(at, m, k, lda, col_begin, n_cols, cp, ri, va, ct, ldc, out_dtype, accumulate, s);
     case TW_BF16:
@@ -571,7 +661,7 @@ cudaError_t launch_exact(const tw_plan *p, const float *at, int64_t m, int64_t l
   if (!hp.tiles.empty() && m > 0) {
     dim3 g((unsigned)((m + 127) / 128), (unsigned)hp.tiles.size(), (unsigned)((hp.wrows + 15) / 16));
     exact_gemm_kernel<<<g, 128, 0, s>>>(p->d_tiles, p->d_kidx, p->d_colids, p->d_wimg, hp.wrows * 128, hp.in_dtype,
-                                        at, m, lda, ct, ldc);
+                                        p->d_w32, p->d_w32_off, at, m, lda, ct, ldc);
   }
   return cudaGetLastError();
 }

@@ -17,6 +17,7 @@ cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *
 cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t k, int64_t lda, int64_t col_begin, int64_t n_cols,
                         const int32_t *cp, const int32_t *ri, const float *va, void *ct, int64_t ldc, int out_dtype,
                         int accumulate, cudaStream_t s);
+cudaError_t launch_prep_split(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, cudaStream_t s);
 cudaError_t launch_exact(const tw_plan *p, const float *at, int64_t m, int64_t lda, float *ct, int64_t ldc,
                          cudaStream_t s);
 cudaError_t launch_prune_means(const double *s, int64_t k, int64_t n, const int32_t *cols, const int64_t *off,
@@ -77,6 +78,23 @@ int upload(T **dst, const std::vector<T> &src) {
 }
 
 int out_size(int dtype) { return dtype == TW_F32 ? 4 : 2; }
+
+// Makes the plan's GPU current for the lifetime of the guard (schedules are
+// uploaded and kernels launched on the device that holds the plan, whatever
+// device the caller has current), restoring the caller's device after.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (dev < 0) return;
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 void free_schedule(tw_dev_schedule &ds) {
   cudaFree(ds.units);
@@ -142,26 +160,34 @@ int tw_device_sm_count(int *sms) {
   return sm_count_of_current(sms, &major);
 }
 
-int tw_plan_create(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off, const int32_t *col_ids,
-                   const uint32_t *row_mask_words, const float *subs, const int64_t *sub_off, int in_dtype,
-                   int64_t col_begin, int64_t col_end, tw_plan **out) {
+int tw_plan_create_ex(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off, const int32_t *col_ids,
+                      const uint32_t *row_mask_words, const float *subs, const int64_t *sub_off, int in_dtype,
+                      int64_t col_begin, int64_t col_end, int flags, tw_plan **out) {
   clear_error();
   if (!out) return fail(TW_ERR_ARG, "null out");
   *out = nullptr;
   tw_plan *p = new (std::nothrow) tw_plan();
   if (!p) return fail(TW_ERR_NOMEM, "out of host memory");
   int rc = build_host_plan(k, n, g, n_tiles, col_off, col_ids, row_mask_words, subs, sub_off, in_dtype, col_begin,
-                           col_end, p->host);
+                           col_end, p->host, flags);
   if (rc) { delete p; return rc; }
   cudaGetDevice(&p->device);
   if ((rc = upload(&p->d_tiles, p->host.tiles)) || (rc = upload(&p->d_kidx, p->host.kidx)) ||
       (rc = upload(&p->d_colids, p->host.colids)) || (rc = upload(&p->d_zero, p->host.zero_rows)) ||
-      (rc = upload(&p->d_wimg, p->host.wimg))) {
+      (rc = upload(&p->d_wimg, p->host.wimg)) || (rc = upload(&p->d_w32, p->host.w32)) ||
+      (rc = upload(&p->d_w32_off, p->host.w32_off))) {
     tw_plan_destroy(p);
     return rc;
   }
   *out = p;
   return TW_OK;
+}
+
+int tw_plan_create(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off, const int32_t *col_ids,
+                   const uint32_t *row_mask_words, const float *subs, const int64_t *sub_off, int in_dtype,
+                   int64_t col_begin, int64_t col_end, tw_plan **out) {
+  return tw_plan_create_ex(k, n, g, n_tiles, col_off, col_ids, row_mask_words, subs, sub_off, in_dtype, col_begin,
+                           col_end, 0, out);
 }
 
 int tw_plan_build_host(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,
@@ -191,6 +217,8 @@ int tw_plan_destroy(tw_plan *p) {
   cudaFree(p->d_colids);
   cudaFree(p->d_zero);
   cudaFree(p->d_wimg);
+  cudaFree(p->d_w32);
+  cudaFree(p->d_w32_off);
   for (auto &kv : p->sched) free_schedule(kv.second);
   if (prev != p->device) cudaSetDevice(prev);
   delete p;
@@ -285,6 +313,8 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   clear_error();
   if (!p) return fail(TW_ERR_ARG, "null plan");
   if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan (tw_plan_build_host) cannot run on the GPU");
+  DeviceGuard guard(p->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice(plan device)");
   if (out_dtype != TW_F32 && out_dtype != TW_BF16 && out_dtype != TW_F16) return fail(TW_ERR_ARG, "bad out_dtype");
   if (m < 0) return fail(TW_ERR_DIMENSION, "M must be >= 0");
   if (m == 0) return TW_OK;
@@ -357,7 +387,11 @@ int tw_gemm_exact(const tw_plan *p, const float *at, int64_t m, int64_t lda, flo
   clear_error();
   if (!p) return fail(TW_ERR_ARG, "null plan");
   if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan cannot run on the GPU");
+  DeviceGuard guard(p->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice(plan device)");
   if (m < 0 || lda < m || ldc < m) return fail(TW_ERR_DIMENSION, "bad M / lda / ldc");
+  if (p->host.flags & TW_PLAN_SPLIT3)
+    return fail(TW_ERR_ARG, "tw_gemm_exact needs a plain plan (TW_PLAN_SPLIT3 plans hold 3 k_i rows per tile)");
   int sms = 0;
   int rc = require_sm100(&sms);
   if (rc) return rc;
@@ -405,6 +439,21 @@ int tw_prep_activations(const float *a, int64_t m, int64_t k, int layout, void *
   return TW_OK;
 }
 
+int tw_prep_activations_split(const float *a, int64_t m, int64_t k, int layout, void *at2, int64_t ldat,
+                              void *stream) {
+  clear_error();
+  if (m < 0 || k < 0) return fail(TW_ERR_DIMENSION, "negative dims");
+  if (layout != TW_ROW_MAJOR && layout != TW_COL_MAJOR) return fail(TW_ERR_ARG, "bad layout");
+  if (ldat < m) return fail(TW_ERR_DIMENSION, "ldat < M");
+  if (m == 0 || k == 0) return TW_OK;
+  int sms = 0;
+  int rc = require_sm100(&sms);
+  if (rc) return rc;
+  cudaError_t e = launch_prep_split(a, m, k, layout, at2, ldat, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tw_prep_activations_split launch");
+  return TW_OK;
+}
+
 int tw_spmm_csc(const void *at, int at_dtype, int64_t k, int64_t m, int64_t lda, int64_t n, const int32_t *col_ptr,
                 const int32_t *row_idx, const float *values, void *ct, int64_t ldc, int out_dtype, int accumulate,
                 void *stream) {
@@ -429,6 +478,9 @@ int tw_gemm_tew(const tw_plan *p, const void *at, int64_t m, int64_t lda, const 
   if (nnz == 0) return tw_gemm(p, at, m, lda, ct, ldc, out_dtype, 0, stream);  // engine.py:194-195
   if (m == 0) return TW_OK;
   const HostPlan &hp = p->host;
+  if (hp.col_end == hp.col_begin) return TW_OK;  // empty column range: nothing to write
+  DeviceGuard guard(p->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice(plan device)");
   if (lda < m || ldc < m) return fail(TW_ERR_DIMENSION, "bad lda / ldc");
   int sms = 0;
   int rc = require_sm100(&sms);

@@ -40,6 +40,8 @@ struct HostPlan {
   int64_t col_begin = 0, col_end = 0;
   int64_t n_tiles = 0;
   int in_dtype = TW_BF16;
+  int flags = 0;       // TW_PLAN_* (tw_b200.h)
+  int64_t a_rows = 0;  // rows of the A^T operand the kept lists index: K, or 2K for TW_PLAN_SPLIT3
   int block_n = 128;   // MMA N tile (<= 256)
   int wrows = 128;     // weight-image rows per k-block (multiple of 16, <= block_n)
   std::vector<TileMeta> tiles;        // live tiles, LPT order
@@ -48,6 +50,8 @@ struct HostPlan {
   std::vector<int32_t> colids;        // block_n entries per live tile (-1 padded)
   std::vector<int32_t> zero_rows;     // output rows written as zeros
   std::vector<uint8_t> wimg;          // swizzled 16-bit weight image
+  std::vector<float> w32;             // TW_PLAN_F32_WEIGHTS: fp32 weights, per live tile nkb*64 x 128 (k-major)
+  std::vector<int64_t> w32_off;       // per live tile offset into w32 (elements)
   int64_t kept_elems = 0, union_k = 0, sum_k = 0, sum_n = 0;
 };
 
@@ -109,7 +113,7 @@ struct GemmArgs {
 int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,
                     const int32_t *col_ids, const uint32_t *row_mask_words, const float *subs,
                     const int64_t *sub_off, int in_dtype, int64_t col_begin, int64_t col_end,
-                    HostPlan &hp);
+                    HostPlan &hp, int flags = 0);
 
 uint16_t f32_to_bf16_rne(float f);
 uint16_t f32_to_f16_rne(float f);
@@ -135,6 +139,8 @@ struct tw_plan {
   int32_t *d_colids = nullptr;
   int32_t *d_zero = nullptr;
   uint8_t *d_wimg = nullptr;
+  float *d_w32 = nullptr;        // TW_PLAN_F32_WEIGHTS
+  int64_t *d_w32_off = nullptr;
   mutable std::mutex sched_mu;
   mutable std::map<std::tuple<int64_t, int, int>, tw_dev_schedule> sched;  // (M, out bytes, zero rows on)
 };

@@ -61,8 +61,11 @@ static inline bool bit_of(const uint32_t *words, int64_t i) { return (words[i >>
 int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int64_t *col_off,
                     const int32_t *col_ids, const uint32_t *row_mask_words, const float *subs,
                     const int64_t *sub_off, int in_dtype, int64_t col_begin, int64_t col_end,
-                    HostPlan &hp) {
+                    HostPlan &hp, int flags) {
   if (k < 1 || n < 1 || g < 1) return fail(TW_ERR_DIMENSION, "bad pattern dims");
+  if (flags & ~(TW_PLAN_SPLIT3 | TW_PLAN_F32_WEIGHTS)) return fail(TW_ERR_ARG, "unknown plan flags");
+  const bool split = (flags & TW_PLAN_SPLIT3) != 0;
+  if (split && in_dtype != TW_BF16) return fail(TW_ERR_ARG, "TW_PLAN_SPLIT3 needs TW_BF16 operands");
   if (g > 256) return fail(TW_ERR_UNSUPPORTED, "tile width G > 256 is not supported by the sm_100a kernel");
   if (in_dtype != TW_BF16 && in_dtype != TW_F16) return fail(TW_ERR_ARG, "in_dtype must be TW_BF16 or TW_F16");
   if (col_begin < 0 || col_end > n || col_begin > col_end) return fail(TW_ERR_DIMENSION, "bad column range");
@@ -71,6 +74,8 @@ int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int6
   hp = HostPlan{};
   hp.k = k; hp.n = n; hp.g = g; hp.n_tiles = n_tiles; hp.in_dtype = in_dtype;
   hp.col_begin = col_begin; hp.col_end = col_end;
+  hp.flags = flags;
+  hp.a_rows = split ? 2 * k : k;
   hp.block_n = g <= 128 ? 128 : 256;
 
   struct Live { int32_t src; int64_t j0, j1; int64_t k_i; std::vector<int32_t> rows; };
@@ -114,22 +119,34 @@ int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int6
     return wa != wb ? wa > wb : a.src < b.src;
   });
   for (int64_t i = 0; i < k; ++i) hp.union_k += union_rows[(size_t)i];
+  if (split) hp.union_k *= 2;  // the high and the low rows of every kept k
   for (int64_t c = 0; c < col_end - col_begin; ++c)
     if (!covered[(size_t)c]) hp.zero_rows.push_back((int32_t)c);
 
   const int bytes_per_kb = hp.wrows * 128;
+  // TW_PLAN_SPLIT3 (fp32-faithful tensor-core mode): with A = Ah + Al and
+  // W = Wh + Wl split into bf16 high / low parts (x = rn(x), rn(x - rn(x))),
+  // A.W ~= Ah.Wh + Al.Wh + Ah.Wl (the dropped Al.Wl is ~2^-18 relative).  The
+  // three products are one TW GEMM over 3 k_i kept rows per tile: kept rows r
+  // of A^T (= Ah) with Wh, rows r + K (= Al, the second half of the 2K-row
+  // split operand tw_prep_activations_split writes) with Wh, rows r with Wl.
+  const int reps = split ? 3 : 1;
   for (const Live &L : live) {
     TileMeta m{};
     const int64_t n_i = L.j1 - L.j0;
+    const int64_t kx = L.k_i * reps;  // kept rows as the kernel sees them
     m.n_i = (int32_t)n_i;
-    m.k_i = (int32_t)L.k_i;
-    m.k16 = (int32_t)((L.k_i + 15) / 16);
-    m.nkb = (int32_t)((L.k_i + 63) / 64);
+    m.k_i = (int32_t)kx;
+    m.k16 = (int32_t)((kx + 15) / 16);
+    m.nkb = (int32_t)((kx + 63) / 64);
     m.kidx_off = (int32_t)hp.kidx.size();
     m.col_off = (int32_t)hp.colids.size();
     m.w_off = (int64_t)hp.wimg.size();
-    for (int64_t r = 0; r < (int64_t)m.nkb * 64; ++r)
-      hp.kidx.push_back(r < L.k_i ? L.rows[(size_t)r] : (int32_t)k);  // pad: OOB row -> TMA zero fill
+    for (int64_t r = 0; r < (int64_t)m.nkb * 64; ++r) {
+      int32_t idx = (int32_t)hp.a_rows;  // pad: out-of-range row -> zeros
+      if (r < kx) idx = L.rows[(size_t)(r % L.k_i)] + (r / L.k_i == 1 ? (int32_t)k : 0);
+      hp.kidx.push_back(idx);
+    }
     const int64_t c0 = col_off[L.src];
     for (int64_t j = 0; j < hp.block_n; ++j)
       hp.colids.push_back(j < n_i ? (int32_t)(col_ids[c0 + L.j0 + j] - col_begin) : -1);
@@ -149,15 +166,36 @@ int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int6
         for (int c = 0; c < 8; ++c) {
           uint16_t *dst = (uint16_t *)(blk + j * 128 + ((c ^ (j & 7)) * 16));
           for (int e = 0; e < 8; ++e) {
-            int64_t kk = (int64_t)kb * 64 + c * 8 + e;
-            float v = kk < ktile ? colv[kk] : 0.0f;
-            dst[e] = in_dtype == TW_BF16 ? f32_to_bf16_rne(v) : f32_to_f16_rne(v);
+            const int64_t kk = (int64_t)kb * 64 + c * 8 + e;
+            if (kk >= kx) { dst[e] = 0; continue; }
+            const float v = colv[kk % ktile];
+            if (!split) {
+              dst[e] = in_dtype == TW_BF16 ? f32_to_bf16_rne(v) : f32_to_f16_rne(v);
+            } else {
+              const uint16_t hi = f32_to_bf16_rne(v);
+              if (kk < 2 * ktile) {
+                dst[e] = hi;
+              } else {  // low part: v - hi exactly representable in fp32
+                const uint32_t hb = (uint32_t)hi << 16;
+                float hv;
+                std::memcpy(&hv, &hb, 4);
+                dst[e] = f32_to_bf16_rne(v - hv);
+              }
+            }
           }
         }
       }
     }
-    hp.kept_elems += L.k_i * n_i;
-    hp.sum_k += L.k_i;
+    if (flags & TW_PLAN_F32_WEIGHTS) {  // the reference's own fp32 weights, for tw_gemm_exact
+      hp.w32_off.push_back((int64_t)hp.w32.size());
+      const int64_t rows32 = (ktile + 63) / 64 * 64;
+      hp.w32.resize(hp.w32.size() + (size_t)(rows32 * 128), 0.0f);
+      float *w = hp.w32.data() + hp.w32_off.back();
+      for (int64_t kk = 0; kk < ktile; ++kk)
+        for (int64_t j = 0; j < n_i; ++j) w[kk * 128 + j] = sub[(L.j0 + j) * ktile + kk];
+    }
+    hp.kept_elems += L.k_i * n_i;  // the reference's kept elements (FLOP count), not the split's 3x
+    hp.sum_k += kx;
     hp.sum_n += n_i;
     hp.tiles.push_back(m);
     hp.src_tile.push_back(L.src);
@@ -306,6 +344,8 @@ int tw_plan_get_info(const tw_plan *plan, tw_plan_info *info) {
   info->block_n = hp.block_n;
   info->wimg_bytes = (int64_t)hp.wimg.size();
   info->in_dtype = hp.in_dtype;
+  info->flags = hp.flags;
+  info->a_rows = hp.a_rows;
   return TW_OK;
 }
 

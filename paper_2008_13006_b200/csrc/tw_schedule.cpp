@@ -203,14 +203,17 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
       for (int kb = 0; kb < t.nkb; ++kb) {
         for (int r = 0; r < 64; ++r) {
           const int32_t idx = hp.kidx[(size_t)t.kidx_off + (size_t)kb * 64 + (size_t)r];
-          s.stream.push_back(kb * 64 + r < t.k_i && idx < hp.k ? idx : -1);
+          s.stream.push_back(kb * 64 + r < t.k_i && idx < hp.a_rows ? idx : -1);
         }
         const int64_t woff = t.w_off + kb * wbytes;
         if (woff > INT32_MAX) return fail(TW_ERR_UNSUPPORTED, "weight image larger than 2 GiB");
         const int32_t nk = std::min(4, t.k16 - kb * 4);
         s.stream.insert(s.stream.end(),
                         {(int32_t)woff, un[1], un[2] | (nk << 4) | (n_mma << 8),
-                         (u - s.off[(size_t)c]) | (kb == 0 ? 1 << 16 : 0) | (kb == t.nkb - 1 ? 1 << 17 : 0)});
+                         // unit ordinal (tracing only) masked to 16 bits: bits 16/17 are
+                         // the first/last-block flags the MMA warp acts on
+                         ((u - s.off[(size_t)c]) & 0xffff) | (kb == 0 ? 1 << 16 : 0) |
+                             (kb == t.nkb - 1 ? 1 << 17 : 0)});
         ++n_stages;
       }
     }

@@ -138,10 +138,21 @@ def as_dense(a) -> DenseMatrix:
 
 
 def as_csc(s) -> CscMatrix:
+    """Accept this package's CscMatrix or the reference's (converted once and
+    cached on the immutable source object, so device copies and merged TEW
+    plans keyed on the converted matrix are reused across calls)."""
     if isinstance(s, CscMatrix):
         return s
-    return CscMatrix(int(s.rows), int(s.cols), np.asarray(s.col_ptr, np.uint32).copy(),
-                     np.asarray(s.row_idx, np.uint32).copy(), np.asarray(s.values, np.float32).copy())
+    cached = getattr(s, "_tw_b200_csc", None)
+    if cached is not None:
+        return cached
+    out = CscMatrix(int(s.rows), int(s.cols), np.asarray(s.col_ptr, np.uint32).copy(),
+                    np.asarray(s.row_idx, np.uint32).copy(), np.asarray(s.values, np.float32).copy())
+    try:
+        object.__setattr__(s, "_tw_b200_csc", out)
+    except Exception:  # objects without a __dict__: convert every call
+        pass
+    return out
 
 
 def transpose(m: DenseMatrix) -> DenseMatrix:

@@ -14,6 +14,7 @@ against fixtures written by the reference).
 
 from __future__ import annotations
 
+from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
@@ -167,3 +168,87 @@ def prune_stage(w, scores, s_t: float, g: int, apriori=None, prev: Optional[Tile
     pruned_set[pruned_rows] = True
     tiles = [Tile(c.astype(np.int32), ~pruned_set[t * k:(t + 1) * k]) for t, c in enumerate(col_groups)]
     return TilePattern(k, n, g, tuple(tiles))
+
+
+# ---------------------------------------------------------------- TEW overlay
+# The input definition of the TEW path (gemm_tew): which pruned weights come
+# back as an element-wise CSC overlay.  pruning.py:132-144 (TewConfig),
+# :147-159 (score maps), :527-561 (tew_overlay).
+
+@dataclass(frozen=True)
+class ScoreMap:
+    """Per-element importance scores (K x N, float64, nonnegative, frozen) --
+    pruning.py:28-47."""
+
+    scores: np.ndarray
+
+    def __post_init__(self) -> None:
+        s = _scores_array(self.scores)
+        object.__setattr__(self, "scores", s)
+        s.setflags(write=False)
+
+    @property
+    def shape(self) -> tuple:
+        return self.scores.shape
+
+
+def magnitude_scores(w) -> ScoreMap:
+    """|w| in float64 (pruning.py:156-159): the score map when there are no
+    gradients."""
+    return ScoreMap(np.abs(as_dense(w).array().astype(np.float64)))
+
+
+@dataclass(frozen=True)
+class TewConfig:
+    """TW pruning at alpha + delta plus a delta fraction of the pruned
+    elements restored element-wise (pruning.py:132-144)."""
+
+    alpha: float
+    delta: float
+
+    def __post_init__(self) -> None:
+        if not (0.0 <= self.delta < self.alpha + self.delta <= 1.0):
+            raise ConfigError(f"need 0 <= delta < alpha+delta <= 1, got alpha={self.alpha} delta={self.delta}")
+
+
+def _restore_order(scores_flat: np.ndarray, device) -> np.ndarray:
+    """Positions of `scores_flat` by descending score, ties by ascending
+    position -- the reference's np.lexsort((idx, -s)) order.  On the GPU a
+    stable descending sort keeps equal scores in position order, which is
+    exactly that tie rule; without CUDA (host-side packing tools) numpy's
+    stable argsort of -s gives the same permutation."""
+    if torch is not None and torch.cuda.is_available() and scores_flat.size > 0:
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        s = torch.from_numpy(np.ascontiguousarray(scores_flat)).to(dev)
+        return torch.sort(s, descending=True, stable=True).indices.cpu().numpy()
+    return np.argsort(-scores_flat, kind="stable")
+
+
+def tew_overlay(w, scores, pattern: TilePattern, cfg: TewConfig, tol: float = 0.05, *, device=None):
+    """pruning.py:527-561: restore the floor(delta*K*N) highest-scored
+    elements the pattern prunes -- in pruned columns too (SURVEY finding 4) --
+    as a CSC overlay holding their original values; the pattern is returned
+    unchanged.  Raises ConfigError when the pattern's sparsity is not
+    alpha + delta within `tol`, or when delta asks for more elements than
+    are pruned; DimensionError on shape mismatches."""
+    from .matrix import to_csc
+    from .pattern import pattern_stats
+
+    w = as_dense(w)
+    s = _scores_array(scores)
+    if w.shape != s.shape:
+        raise DimensionError(f"weight {w.shape} and scores {s.shape} differ")
+    if (pattern.k, pattern.n) != w.shape:
+        raise DimensionError("pattern does not match weight matrix")
+    sparsity = pattern_stats(pattern, m=1).sparsity
+    if abs(sparsity - (cfg.alpha + cfg.delta)) > tol:
+        raise ConfigError(f"pattern sparsity {sparsity:.4f} is not alpha+delta={cfg.alpha + cfg.delta:.4f} "
+                          f"within {tol}")
+    count = exact_count(cfg.delta, pattern.k * pattern.n)
+    pruned_flat = np.flatnonzero(~_keep_mask(pattern).ravel())
+    if count > pruned_flat.size:
+        raise ConfigError(f"delta asks to restore {count} elements but only {pruned_flat.size} are pruned")
+    chosen = pruned_flat[_restore_order(s.ravel()[pruned_flat], device)[:count]]
+    restore = np.zeros(pattern.k * pattern.n, dtype=bool)
+    restore[chosen] = True
+    return pattern, to_csc(w, restore.reshape(pattern.k, pattern.n))

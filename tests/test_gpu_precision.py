@@ -1,0 +1,174 @@
+"""The drop-in's precision modes replayed against the reference's OWN
+acceptance tests, with the reference's own objects.
+
+`tilewise` is the unmodified reference installed in baseline/_ref (it travels
+to the GPU box with the snapshot).  The cases
+below regenerate test_acceptance.py's inputs with the same seeds and pass the
+reference's DenseMatrix / CompactTileSet / CscMatrix objects straight into
+paper_2008_13006_b200's gemm_tw / gemm_tew / spmm_csc (duck typing), as a
+user who swaps the import would:
+
+  c01 (test_acceptance.py:63-81): 200 random unrounded fp32 triples, G in
+      {32, 64, 128}, s in {0, .25, .5, .75, .9}: gemm_tw within 1e-4*K of the
+      reference's zero-fill dense oracle -- precision "fp32" (split-bf16
+      tensor cores, the drop-in default) and "exact" (bit-identical).
+  c02 (test_acceptance.py:84-120): 50 TEW cases incl. delta=0 and full
+      restore: gemm_tew == gemm_tw + spmm_csc element for element.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2008_13006_b200 as tw  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "tilewise")):
+        pytest.skip("reference not installed in baseline/_ref")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_tw")
+    sys.path.insert(0, path)
+    try:
+        import tilewise
+    finally:
+        sys.path.remove(path)
+    return tilewise
+
+
+def _random_dense(ref, rows, cols, rng):
+    return ref.DenseMatrix.from_array(rng.standard_normal((rows, cols)).astype(np.float32))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "exact"])
+def test_c01_oracle_equivalence_through_drop_in(ref, precision):
+    rng = np.random.default_rng(1001)
+    sparsities = (0.0, 0.25, 0.5, 0.75, 0.9)
+    gs = (32, 64, 128)
+    worst = 0.0
+    for case in range(200):
+        m, k, n = (int(rng.integers(64, 513)) for _ in range(3))
+        g = int(gs[rng.integers(len(gs))])
+        s = float(sparsities[rng.integers(len(sparsities))])
+        a = _random_dense(ref, m, k, rng)
+        w = _random_dense(ref, k, n, rng)
+        p = ref.random_uniform_pattern(k, n, g, s, seed=2000 + case)
+        got = tw.gemm_tw(a, ref.compact(w, p), precision=precision)
+        want = ref.gemm_dense(a, ref.zero_fill(w, p))
+        assert int(got.layout) == int(ref.Layout.COL_MAJOR)
+        diff = float(np.abs(got.array() - want.array()).max())
+        worst = max(worst, diff / k)
+        assert diff <= 1e-4 * k, f"case {case}: m={m} k={k} n={n} g={g} s={s} diff={diff}"
+        if precision == "exact":  # the reference's own gemm_tw bits
+            ref_tw = ref.gemm_tw(a, ref.compact(w, p))
+            assert np.array_equal(got.data, ref_tw.data), f"case {case} not bit-exact"
+    if precision == "fp32":
+        assert worst < 1e-6, worst  # far inside the bar: ~2^-17 per product
+
+
+def test_bf16_precision_is_below_the_fp32_bar_on_raw_inputs(ref):
+    """Why the default is "fp32": bf16 operands on unrounded fp32 data miss
+    c01's 1e-4*K (max-abs) bar at these sizes, the split mode does not."""
+    rng = np.random.default_rng(7)
+    m, k, n = 512, 512, 512
+    a = _random_dense(ref, m, k, rng)
+    w = _random_dense(ref, k, n, rng)
+    p = ref.random_uniform_pattern(k, n, 128, 0.0, seed=1)
+    want = ref.gemm_dense(a, ref.zero_fill(w, p)).array()
+    d16 = np.abs(tw.gemm_tw(a, ref.compact(w, p), precision="bf16").array() - want).max()
+    d32 = np.abs(tw.gemm_tw(a, ref.compact(w, p), precision="fp32").array() - want).max()
+    assert d32 <= 1e-4 * k < d16
+
+
+@pytest.mark.parametrize("precision", ["fp32", "exact"])
+def test_c02_tew_linearity_through_drop_in(ref, precision):
+    rng = np.random.default_rng(1002)
+    for case in range(50):
+        m = int(rng.integers(16, 129))
+        k = int(rng.integers(32, 257))
+        n = int(rng.integers(32, 257))
+        g = int((16, 32, 64)[rng.integers(3)])
+        s = float(rng.uniform(0.3, 0.9))
+        a = _random_dense(ref, m, k, rng)
+        w = _random_dense(ref, k, n, rng)
+        p = ref.random_uniform_pattern(k, n, g, s, seed=3000 + case)
+        tiles = ref.compact(w, p)
+        pruned_frac = 1.0 - p.keep_mask().mean()
+        if case % 3 == 0:
+            delta = 0.0
+        elif case % 3 == 1:
+            delta = pruned_frac  # full restore
+        else:
+            delta = float(rng.uniform(0.0, pruned_frac) if pruned_frac else 0.0)
+        if delta == 0.0:
+            csc = ref.to_csc(w, np.zeros((k, n), dtype=bool))
+        else:
+            cfg = ref.TewConfig(alpha=max(pruned_frac - delta, 0.0) + 0.01, delta=delta)
+            _, csc = ref.tew_overlay(w, ref.magnitude_scores(w), p, cfg, tol=0.05)
+        got = tw.gemm_tew(a, tiles, csc, precision=precision).array()
+        explicit = tw.gemm_tw(a, tiles, precision=precision).array() + tw.spmm_csc(a, csc).array()
+        assert np.array_equal(got, explicit), f"case {case}: not the explicit sum"
+        if precision == "exact":
+            assert np.array_equal(got, ref.gemm_tew(a, tiles, csc).array()), f"case {case}: not the reference's bits"
+        if delta == pruned_frac and pruned_frac > 0.0:
+            dense = ref.gemm_dense(a, w).array()
+            assert float(np.abs(got - dense).max()) <= 1e-4 * k, f"case {case}"
+
+
+def test_device_plans_per_precision_agree(ref):
+    """TwPlan(precision=...).prep + gemm on device tensors: the three modes
+    against the reference on one unrounded case."""
+    rng = np.random.default_rng(11)
+    m, k, n = 300, 200, 260
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    w = rng.standard_normal((k, n)).astype(np.float32)
+    p = ref.random_uniform_pattern(k, n, 64, 0.5, seed=5)
+    ts = ref.compact(ref.DenseMatrix.from_array(w), p)
+    want = ref.gemm_tw(ref.DenseMatrix.from_array(a), ts).data.reshape(n, m)
+    a_dev = torch.from_numpy(a).cuda()
+    res = {}
+    for prec in ("bf16", "fp32", "exact"):
+        plan = tw.TwPlan(ts, precision=prec)
+        op = plan.prep(a_dev)
+        assert op.shape[0] == (2 * k if prec == "fp32" else k)
+        res[prec] = plan.gemm(op).cpu().numpy()
+    rel = lambda x: float(np.linalg.norm(x - want) / np.linalg.norm(want))  # noqa: E731
+    assert np.array_equal(res["exact"], want)
+    assert rel(res["fp32"]) < 2e-6
+    assert 1e-4 < rel(res["bf16"]) < 1e-2
+
+
+def test_execute_batched_drop_in(ref):
+    """engine.py:84-123 with the reference's own TileTasks / BatchGroups
+    (from its _plan_tasks + group_by_shape): one persistent launch over the
+    stacked gathered operands.  precision="exact" gives the reference's bits;
+    "fp32" is within its acceptance bar."""
+    rng = np.random.default_rng(21)
+    m, k, n = 200, 300, 500
+    a = _random_dense(ref, m, k, rng)
+    w = _random_dense(ref, k, n, rng)
+    p = ref.random_uniform_pattern(k, n, 64, 0.6, seed=9)
+    tiles = ref.compact(w, p)
+    tasks = ref.engine._plan_tasks(a, tiles)
+    groups = ref.group_by_shape(tasks)
+    want = ref.execute_batched(groups, n, workers=2)
+    assert np.array_equal(tw.execute_batched(groups, n, workers=3, precision="exact"), want)
+    got = tw.execute_batched(groups, n, precision="fp32")
+    assert float(np.abs(got - want).max()) <= 1e-4 * k
+    # our own task API on the same data
+    ours = tw.group_by_shape([tw.TileTask(t.index, tw.gather_rows(np.ascontiguousarray(a.array().T), tt.row_mask_words),
+                                          t.b_sub, t.out_rows) for t, tt in zip(tasks, [tiles.tiles[t.index] for t in tasks])])
+    assert np.array_equal(tw.execute_batched(ours, n, precision="exact"), want)

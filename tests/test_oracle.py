@@ -86,6 +86,28 @@ def test_oracle_full_size_hash_matches_reference(name):
     assert sha(ct) == h["gemm_tw_sha256"]
 
 
+SHAPE_CASES = ["C5_s0", "C5_s75", "C5_s90", "VGG_conv1_1_s50", "VGG_conv1_2_s75", "VGG_conv4_2_s50", "NMT_lstm_s75"]
+
+
+@pytest.mark.parametrize("name", SHAPE_CASES)
+def test_oracle_baseline_shapes_hash_matches_reference(name):
+    """C5 BERT-large, VGG-16 im2col and the NMT LSTM gate shape (reduced M):
+    the C oracle reproduces the reference's gemm_tw bit for bit
+    (tests/golden/make_golden_shapes.py), and the oracle pattern generator
+    reproduces the reference's tile structure."""
+    h = gio.load("golden_hashes_shapes.json")[name]
+    m, k, n, g, s = h["dims"]
+    a, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)
+    tiles = p[3]
+    assert len(tiles) == h["tiles"]
+    assert [len(c) for c, _ in tiles] == h["n_i"]
+    assert sorted({int(keep.sum()) for _, keep in tiles}) == h["k_i"]
+    assert len(orc.pruned_columns(p)) == h["pruned_columns"]
+    packed = orc.PackedTiles(orc.compact(w, p), k, n)
+    ct = orc.gemm_tw_ct(np.ascontiguousarray(a.T), packed, threads=orc.max_threads())
+    assert sha(ct) == h["gemm_tw_sha256"]
+
+
 def test_oracle_tew_full_size_hash_matches_reference():
     h = gio.load("golden_hashes.json")["C4"]
     m, k, n, g, s = h["dims"]

@@ -235,3 +235,59 @@ def test_tew_merged_tileset_is_tw_plus_overlay(seed, s, delta):
 
 def ts_kept(ts):
     return sum(t.sub_matrix.rows * t.sub_matrix.cols for t in ts.tiles)
+
+
+def test_tew_overlay_in_product_matches_reference_hash():
+    """tew_overlay / TewConfig / magnitude_scores in the product (pruning.py:
+    132-159, :527-561 of the reference): the C4 overlay is bit-identical to
+    the one the reference wrote (csc_sha256 from tests/golden/make_golden.py),
+    and the small golden cases' overlays match the reference's arrays."""
+    import hashlib
+
+    from tests import golden_io as gio
+
+    h = gio.load("golden_hashes.json")["C4"]
+    m, k, n, g, s = h["dims"]
+    _, w, p = orc.bench_inputs(m, k, n, g, s, seed=42)  # A is drawn first: same M
+    pat = tw.TilePattern(k, n, g, tuple(tw.Tile(c, keep) for c, keep in p[3]))
+    sp = tw.pattern_stats(pat, m=1).sparsity
+    W = tw.DenseMatrix.from_array(w)
+    out_p, csc = tw.tew_overlay(W, tw.magnitude_scores(W), pat, tw.TewConfig(alpha=sp - h["delta"], delta=h["delta"]))
+    assert out_p is pat and csc.nnz == h["nnz"]
+    hh = hashlib.sha256()
+    for arr in (csc.col_ptr, csc.row_idx, csc.values):
+        hh.update(np.ascontiguousarray(arr).tobytes())
+    assert hh.hexdigest() == h["csc_sha256"]
+    for name in gio.small_names():
+        c = gio.small_case(name)
+        if "csc" not in c:
+            continue
+        pat = tw.TilePattern(c["k"], c["n"], c["g"], tuple(tw.Tile(cc, keep) for cc, keep in c["pattern"][3]))
+        sp = tw.pattern_stats(pat, m=1).sparsity
+        W = tw.DenseMatrix.from_array(c["w"])
+        delta = float(c["delta"])
+        _, got = tw.tew_overlay(W, tw.magnitude_scores(W), pat, tw.TewConfig(alpha=sp - delta, delta=delta))
+        cp, ri, va = c["csc"]
+        assert np.array_equal(got.col_ptr, cp) and np.array_equal(got.row_idx, ri) and np.array_equal(got.values, va)
+    with pytest.raises(tw.ConfigError):
+        tw.TewConfig(alpha=0.5, delta=0.6)
+    with pytest.raises(tw.ConfigError):  # sparsity far from alpha + delta
+        tw.tew_overlay(W, tw.magnitude_scores(W), pat, tw.TewConfig(alpha=0.01, delta=0.01))
+
+
+def test_reference_engine_task_api_names():
+    """engine.py:24-81 names the drop-in exports: TileTask / BatchGroup /
+    gather_rows / group_by_shape (host semantics; execute_batched runs on
+    the GPU, tests/test_gpu_parity.py)."""
+    rng = np.random.default_rng(4)
+    at = rng.standard_normal((40, 7)).astype(np.float32)
+    keep = rng.random(40) > 0.5
+    words = tw.pack_mask_words(keep)
+    assert np.array_equal(tw.gather_rows(at, words), at[keep])
+    full = tw.pack_mask_words(np.ones(40, bool))
+    assert tw.gather_rows(at, full) is at and tw.gather_rows(at, full, force_copy=True) is not at
+    mk = lambda i, kk, nn: tw.TileTask(i, np.zeros((kk, 7), np.float32), np.zeros((kk, nn), np.float32, order="F"),  # noqa: E731
+                                       np.arange(nn, dtype=np.int64))
+    groups = tw.group_by_shape([mk(0, 4, 8), mk(1, 9, 16), mk(2, 4, 16), mk(3, 30, 8)])
+    assert [g.n_i for g in groups] == [8, 16] and [t.index for t in groups[0].tasks] == [0, 3]
+    assert groups[0].flops == 2 * 7 * (4 * 8 + 30 * 8)

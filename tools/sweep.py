@@ -9,6 +9,9 @@ Rows:
        N = Cout) at 50% and 75% TW
   C4   TEW on BERT-base FC1: 76.5% TW + 1.5% element-wise overlay (CSC)
   C5   BERT-large FC1 16384x1024x4096, sparsity 0 / .1 / .25 / .5 / .75 / .9
+  NMT  LSTM gate GEMM of a 512-unit layer, [x;h] (K=1024) -> 4 gates (N=2048),
+       4096 tokens, at 50 / 75 / 90% -- an assumed shape (PAPER.md:626-627
+       gives none)
 
 Per row: TW kernel time (CUDA events, mean of `reps` launches over rotating
 output buffers when the output is smaller than 2x L2; calls graph-captured and replayed), fp32 and fp16 output;
@@ -52,6 +55,8 @@ def rows(quick: bool):
     r = [("C1", 1024, 1024, 1024, 0.50, None), ("C2a", 4096, 768, 3072, 0.75, None),
          ("C2b", 4096, 768, 768, 0.75, None), ("C4-TEW", 4096, 768, 3072, 0.765, 0.015),
          ("C2a-het", 4096, 768, 3072, 0.75, None), ("C5-het@0.75", 16384, 1024, 4096, 0.75, None)]
+    for s in (0.5, 0.75, 0.9):
+        r.append((f"NMT@{s:g}", 4096, 1024, 2048, s, None))
     for s in ([0.0, 0.5, 0.75, 0.9] if quick else [0.0, 0.1, 0.25, 0.5, 0.75, 0.9]):
         r.append((f"C5@{s:g}", 16384, 1024, 4096, s, None))
     vgg = VGG[1::3] if quick else VGG
