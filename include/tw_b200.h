@@ -198,6 +198,10 @@ int tw_gemm_bias(const tw_plan *plan, const void *at, int64_t m, int64_t lda, vo
  * bias may be NULL. */
 #define TW_GEMM_ACCUMULATE 1
 #define TW_GEMM_KEEP_PRUNED 2
+/* Launch without programmatic dependent launch: the kernel starts only after
+ * the previous work in the stream has completed (for isolated timing next to
+ * library GEMMs, which are launched that way). */
+#define TW_GEMM_NO_PDL 4
 int tw_gemm_ex(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
                int flags, const float *bias, int relu, void *stream);
 

@@ -356,6 +356,7 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.M = (int32_t)m;
   a.accumulate = accum ? 1 : 0;
   a.keep_pruned = keep_pruned ? 1 : 0;
+  a.no_pdl = (accumulate & TW_GEMM_NO_PDL) ? 1 : 0;
   a.wbytes = hp.wrows * 128;
   // kind::f16 instruction descriptor: D f32 [4,6)=1, A/B bf16 [7,10)/[10,13)=1
   // (fp16 = 0), A (weights) K-major [15]=0, B (gathered A^T) MN-major [16]=1,

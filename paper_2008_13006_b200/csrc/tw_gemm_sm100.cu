@@ -721,7 +721,7 @@ cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = (pdl && !args.no_pdl) ? 1 : 0;
   e = cudaLaunchKernelEx(&cfg, kern, args);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

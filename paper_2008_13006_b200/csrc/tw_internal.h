@@ -107,6 +107,7 @@ struct GemmArgs {
   int32_t zero_policy; // when the epilogue writes zero rows (kernel comment); env TW_B200_ZERO
   int32_t n_peer;      // replicas of the output on other GPUs (tw_gemm_peers): every store goes to all
   void *peer[7];       //   of them too (NVLink peer / IPC-mapped pointers, same layout and ldc)
+  int32_t no_pdl;     // 1: launch without programmatic stream serialization (TW_GEMM_NO_PDL)
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };
 

@@ -273,7 +273,7 @@ class TwPlan(PackedPlan):
         return out
 
     def gemm(self, at, out=None, out_dtype=None, accumulate=False, stream=None, bias=None, relu=False,
-             write_pruned=True):
+             write_pruned=True, pdl=True):
         """C^T (N x M) = (A * expand(tiles))^T for A^T (K x M) -- engine.py:152-164.
         Pruned columns are exact zeros unless accumulate=True (then they are
         left untouched and kept columns are added into `out`).
@@ -294,7 +294,7 @@ class TwPlan(PackedPlan):
         if (accumulate or not write_pruned) and out is None:
             raise ValueError("accumulate=True / write_pruned=False need out")
         ct = self._out(m, out, out_dtype)
-        flags = (1 if accumulate else 0) | (0 if write_pruned else 2)
+        flags = (1 if accumulate else 0) | (0 if write_pruned else 2) | (0 if pdl else 4)
         bias_ptr = None
         if bias is not None:
             if accumulate:

@@ -215,21 +215,37 @@ class ShardedTwPlan:
             _lib.call("tw_ipc_free", own)
         self._peer.clear()
 
+    def _stream_barrier(self, stream):
+        """All ranks reach this point of their streams before any continues.
+        NCCL: a one-element all-reduce queued on the stream -- a device-side
+        barrier, no host round trip.  gloo (several ranks sharing a device in
+        the CPU/1-GPU tests): host barrier after draining the device."""
+        if dist.get_backend(self.group) == "nccl":
+            flag = self.__dict__.get("_flag")
+            if flag is None:
+                flag = self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+            ctx = torch.cuda.stream(stream) if isinstance(stream, torch.cuda.Stream) else contextlib.nullcontext()
+            with ctx:
+                dist.all_reduce(flag, group=self.group)
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
+
     def _gemm_fused(self, at, out_dtype, stream):
         m = at.shape[1]
         full, dsts, _own, _peers = self._peer_buffers(m, out_dtype)
         width = self.col_range[1] - self.col_range[0]
         # peers are done reading the previous result from their replicas
-        dist.barrier(group=self.group)
+        self._stream_barrier(stream)
         if width and m:
             if at.dtype != self.plan.dtype or at.dim() != 2 or at.shape[0] != self.k:
                 raise DimensionError(f"A^T must be a ({self.k}, M) {self.plan.dtype} CUDA tensor")
             _lib.call("tw_gemm_peers", self.plan._h, at.data_ptr(), m, at.stride(0), ctypes.cast(dsts, ctypes.c_void_p),
                       self.world, m,
-                      _code(out_dtype), _stream_ptr(stream))
-        # every rank's rows have landed in every replica
-        torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.group)
+                      _code(out_dtype), _stream_ptr(stream, self.device))
+        # every rank's kernel (queued before the barrier on its stream) has
+        # finished storing into every replica
+        self._stream_barrier(stream)
         return full[: self.n]
 
     def gemm(self, at, out_dtype=None, stream=None):
