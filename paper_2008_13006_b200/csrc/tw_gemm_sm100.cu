@@ -453,6 +453,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // A^T may be produced by the previous kernel in the stream (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const bool traced = args.trace != nullptr;
+    // (tracing) which producer thread records per-stage cycles: warp 0 (it
+    // also issues the weight TMA) or, with debug bit 65536, warp 1
+    const int tr_thread = (args.debug & 65536) ? 32 : 0;
     for (int i = 0; i < n_st; ++i) {
       const int32_t *slot = ring + (i % kIdxSlots) * kSlotInts;
       const long long c0 = traced ? clock64() : 0;  // SM-clock reads only when tracing
@@ -549,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       ptx::cp_async_mbar_arrive_noinc(&full[stage]);  // also covers the prefetch
       ptx::cp_async_commit();
       if (threadIdx.x == 0) trace_stage(args, i, 0);
-      if (threadIdx.x == 0 && args.trace != nullptr && i < 32) {
+      if (threadIdx.x == tr_thread && args.trace != nullptr && i < 32) {
         const long long c3 = clock64();
         // 4 x 16 bits: wait_empty, wait_idx, index smem loads, issue
         args.trace[(int64_t)gridDim.x * 64 + ((int64_t)blockIdx.x * 32 + i) * 4 + 3] =
