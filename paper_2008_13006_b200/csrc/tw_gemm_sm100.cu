@@ -25,12 +25,15 @@
 //     N = the unit's tokens: ONE MMA per k-step for a 256-token unit.
 //   D (TMEM, fp32): lane = tile column, column = token; 2 x 256 columns
 //     (double-buffered accumulators).
-// Epilogue (8 warps, drain_unit).  tcgen05.ld.32x32b gives each thread 32
-// consecutive tokens of one output column, i.e. a piece of one C^T row: the
-// fused bias / ReLU are per-thread constants, the values are rounded once and
-// staged with 16-byte shared stores, and every warp then writes whole C^T row
-// segments with 16-byte streaming stores (storing straight from registers
-// would put 32 rows in every store instruction: 1.3 TB/s in membench2).
+// Epilogue (8 warps).  tcgen05.ld.32x32b gives each thread 32 consecutive
+// tokens of one output column, i.e. a piece of one C^T row: the fused bias /
+// ReLU are per-thread constants, the values are rounded once and staged with
+// 16-byte shared stores into [tile column][tokens] rows, and the staged rows
+// leave with 1-D TMA bulk stores (drain_unit_bulk: one cp.async.bulk per
+// C^T row piece, issued by lane 0 of every epilogue warp) -- the LSU that
+// carries the producer's cp.async gathers only sees the shared stores.  The
+// accumulate, peer-store and unaligned cases use the LSU path (drain_unit:
+// staging read back, 16-byte streaming stores).
 //
 // Warp roles (416 threads): w0-3 producer (A gather + W bulk copy), w4 MMA
 // issuer + TMEM owner, w5-12 epilogue (TMEM lane quadrant = warp % 4).
@@ -77,10 +80,14 @@ struct Cfg {
   static constexpr uint32_t kBBytes = BN * 128;               // weight block per stage: 16 KB | 32 KB
   static constexpr uint32_t kAccCols = 256;                   // TMEM columns per accumulator
   static constexpr uint32_t kTmemCols = 2 * kAccCols;
-  static constexpr uint32_t kStageBytes = 32768;              // epilogue staging pass buffer; two are used
+  // epilogue staging: a whole unit of 16-bit output (BN <= 128: 128 rows x
+  // 512 B, BN = 256: 256 rows x 256 B) with 16 B of padding per row, so the
+  // 32 rows of one tcgen05.ld land in distinct bank groups; drain_unit's two
+  // 32 KB LSU-path buffers alias the same region
+  static constexpr uint32_t kStagingBytes = 69632;
   static constexpr uint32_t kColBytes = 2 * BN * 4;                     // col-id table, double buffered
   static constexpr uint32_t kZeroBytes = 8192;  // zero source block for TMA zero-row stores
-  static constexpr uint32_t kFixed = 1024 /*align slack*/ + 2 * kStageBytes + kColBytes + 256 /*barriers*/ +
+  static constexpr uint32_t kFixed = 1024 /*align slack*/ + kStagingBytes + kColBytes + 256 /*barriers*/ +
                                      kProducerWarps * kIdxSlots * kSlotInts * 4 + kZeroBytes;
   // as many 64-k pipeline stages as fit next to the epilogue buffers (4 for
   // G <= 128): bytes in flight per SM set the gather throughput
@@ -232,7 +239,7 @@ __device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int la
 //     and, in every pass, tokens [p*2T + h*T, +T): a staged row holds 2T
 //     contiguous tokens.
 //   BN == 256: region h (columns 128h..128h+127); each warp all tokens.
-template <int BN, typename OutT, typename S, int T, bool kPeer>
+template <int BN, typename OutT, typename S, int T, bool kPeer, bool kTrace>
 __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, float *sStage, uint32_t t_acc,
                                            uint64_t *tempty, const TileMeta &t, int m0, int nq, const int32_t *ucol,
                                            int q, int h, int e, int lane, bool vec) {
@@ -304,17 +311,29 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
       const int r = e * WROWS + r0 + lrow;
       const int c = BN <= 128 ? r : r;  // staged row == tile column
       const int tk = p * RT + piece * V;  // token within the unit
-      if (c >= t.n_i || (args.debug & 2) || tk >= toks || m0 + tk >= args.M) continue;
-      float y[V];
+      if (c >= t.n_i || (kTrace && (args.debug & 2)) || tk >= toks || m0 + tk >= args.M) continue;
       const S *srow = buf + r * RT;
+      const int64_t off = (int64_t)ucol[c] * args.ldc + m0 + tk;
+      OutT *grow = out + off;
+      if constexpr (std::is_same<S, OutT>::value) {
+        // 16-bit staging, overwrite: the staged 16 bytes ARE the output (no
+        // unpack / repack)
+        if (!args.accumulate && vec && m0 + tk + V <= args.M) {
+          const uint4 w = reinterpret_cast<const uint4 *>(srow)[(piece & ~7) | ((piece ^ r) & 7)];
+          __stcs(reinterpret_cast<uint4 *>(grow), w);
+          if constexpr (kPeer)
+            for (int d = 0; d < args.n_peer; ++d)
+              __stcs(reinterpret_cast<uint4 *>(reinterpret_cast<OutT *>(args.peer[d]) + off), w);
+          continue;
+        }
+      }
+      float y[V];
 #pragma unroll
       for (int x = 0; x < V; x += 16 / (int)sizeof(S)) {
         const int cc = (piece * V + x) * (int)sizeof(S) / 16;
         const uint4 w = reinterpret_cast<const uint4 *>(srow)[(cc & ~7) | ((cc ^ r) & 7)];
         unpack16<S>(w, y + x);
       }
-      const int64_t off = (int64_t)ucol[c] * args.ldc + m0 + tk;
-      OutT *grow = out + off;
       if (vec && m0 + tk + V <= args.M) {
         uint4 *gp = reinterpret_cast<uint4 *>(grow);
         if (args.accumulate) unpack16_add<OutT>(*gp, y);
@@ -341,11 +360,102 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
   }
 }
 
+// Epilogue of one unit through TMA bulk stores (overwrite, 16-byte aligned
+// output, no peers).  Per pass, every thread loads its TMEM lane's tokens
+// (tcgen05.ld.32x32b, 32 tokens at a time), applies the fused
+// bias / ReLU, rounds once and writes its row piece into the staging rows
+// [tile column][pass tokens] (row stride = piece + 16 B: conflict-free
+// 16-byte shared stores); after one named barrier, lane 0 of warp e issues
+// the 1-D bulk copies of staged rows e, e + 8, ... straight to their C^T rows
+// (col_ids) -- one instruction per row piece, executed by the TMA engine.
+// The next pass (or unit) waits until the bulk copies have READ the staging
+// rows (cp.async.bulk.wait_group.read), not until the writes land.
+//   BN <= 128: 128 rows x 512 B per pass (16-bit: the whole 256-token unit;
+//     fp32: 128 tokens); warp (q, h): rows 32q.., tokens h * pass/2 ..
+//   BN == 256: 256 rows x 256 B per pass; warp (q, h): rows 128h + 32q..
+template <int BN, typename OutT>
+__device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out, uint8_t *sStg, uint32_t t_acc,
+                                                uint64_t *tempty, const TileMeta &t, int m0, int nq,
+                                                const int32_t *ucol, int q, int h, int e, int lane) {
+  constexpr int kRows = BN <= 128 ? 128 : 256;
+  constexpr int kRowBytes = BN <= 128 ? 512 : 256;
+  constexpr int kStride = kRowBytes + 16;
+  constexpr int kPassTok = kRowBytes / (int)sizeof(OutT);
+  constexpr int kWarpTok = BN <= 128 ? kPassTok / 2 : kPassTok;  // tokens per warp per pass
+  constexpr int kLoads = kWarpTok / 32;
+  constexpr int kChunks = 32 * (int)sizeof(OutT) / 16;             // 16-byte chunks per 32 tokens
+  static_assert(kRows * kStride <= 69632, "staging");
+  const int toks = nq * 64;
+  const int n_pass = (toks + kPassTok - 1) / kPassTok;
+  const int region = BN <= 128 ? 0 : h;
+  const int row = region * 128 + q * 32 + lane;  // staged row = tile column of this thread
+  const bool warp_live = region * 128 + q * 32 < t.n_i;
+  const int tw0 = BN <= 128 ? h * kWarpTok : 0;
+  const uint32_t t_base = t_acc + ((uint32_t)(q * 32) << 16) + (uint32_t)(region * 128);
+  float bz = 0.f;
+  if (args.bias != nullptr && row < t.n_i) bz = __ldg(args.bias + ucol[row]);
+  uint8_t *srow = sStg + row * kStride;
+  for (int p = 0; p < n_pass; ++p) {
+    if (lane == 0) ptx::bulk_wait_read<0>();  // earlier bulk stores are done reading the staging rows
+    epi_sync();
+    const int ptok0 = p * kPassTok;
+    if (warp_live) {
+#pragma unroll
+      for (int x = 0; x < kLoads; ++x) {
+        const int tau = ptok0 + tw0 + 32 * x;  // token (within the unit)
+        if (tau >= toks) break;                // warp-uniform
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)tau, v);
+        ptx::tmem_ld_wait();
+        if (args.bias != nullptr) {  // trainer.py:246-248, in fp32 before the one rounding
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float z = __fadd_rn(__uint_as_float(v[i]), bz);
+            if (args.relu) z = fmaxf(z, 0.f);
+            v[i] = __float_as_uint(z);
+          }
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(srow + (tw0 + 32 * x) * (int)sizeof(OutT));
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c)
+          dst[c] = pack16<OutT>(reinterpret_cast<const float *>(v) + c * (16 / (int)sizeof(OutT)));
+      }
+    }
+    if (p == n_pass - 1) {  // every TMEM read of the unit is done: hand the accumulator back
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(tempty);
+    }
+    ptx::fence_proxy_async_smem();  // the staged rows are read by the TMA (async proxy)
+    epi_sync();
+    if (lane == 0) {
+      const int tok_n = min(kPassTok, min(toks - ptok0, args.M - m0 - ptok0));
+      if (tok_n > 0) {
+        const uint32_t bytes = (uint32_t)tok_n * (uint32_t)sizeof(OutT);  // multiple of 16 (bulk_ok)
+        for (int r = e; r < kRows && r < t.n_i; r += 8) {
+          char *g = reinterpret_cast<char *>(out + (int64_t)ucol[r] * args.ldc + m0 + ptok0);
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g),
+                       "r"(ptx::smem_u32(sStg + r * kStride)), "r"(bytes)
+                       : "memory");
+        }
+        ptx::bulk_commit();
+      }
+    }
+  }
+}
+
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
 // committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
+// Experiment knobs (TW_B200_DEBUG) exist only in the profiling instantiation
+// (tw_gemm_traced): the production kernel compiles them out.
+template <bool kTrace>
+__device__ __forceinline__ bool dbg(const GemmArgs &a, int bit) {
+  return kTrace && (a.debug & bit) != 0;
+}
+
+template <bool kTrace>
 __device__ __forceinline__ void trace_evt(const GemmArgs &a, int unit_i, int slot) {
-  if (a.trace != nullptr && unit_i < 8) {
+  if (kTrace && unit_i < 8) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[((int64_t)blockIdx.x * 8 + unit_i) * 8 + slot] = (int64_t)t;
@@ -353,15 +463,16 @@ __device__ __forceinline__ void trace_evt(const GemmArgs &a, int unit_i, int slo
 }
 // per pipeline stage (first 32 of each CTA), after the unit table:
 // slot 0 producer issued, 1 MMA saw it full, 2 MMA committed
+template <bool kTrace>
 __device__ __forceinline__ void trace_stage(const GemmArgs &a, int s, int slot) {
-  if (a.trace != nullptr && s < 32) {
+  if (kTrace && s < 32) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[(int64_t)gridDim.x * 64 + ((int64_t)blockIdx.x * 32 + s) * 4 + slot] = (int64_t)t;
   }
 }
 
-template <int BN, typename OutT, bool kPeer>
+template <int BN, typename OutT, bool kPeer, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid_constant__ GemmArgs args) {
   using C = Cfg<BN>;
   constexpr int TB = C::TB;
@@ -374,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::kStages * C::kABytes;
   float *sStage = reinterpret_cast<float *>(sB + C::kStages * C::kBBytes);
-  int32_t *sCol = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(sStage) + 2 * C::kStageBytes);
+  int32_t *sCol = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(sStage) + C::kStagingBytes);
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sCol) + C::kColBytes);
   uint64_t *empty = full + C::kStages;
   uint64_t *tfull = empty + C::kStages;
@@ -391,8 +502,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   const int n_st = __ldg(args.stream_off + blockIdx.x + 1) - s_begin;
 
   if (threadIdx.x == 0) {
-    trace_evt(args, 7, 0);  // CTA start
-    if (args.trace != nullptr) args.trace[((int64_t)blockIdx.x * 8 + 7) * 8 + 2] = (int64_t)clock64();
+    trace_evt<kTrace>(args, 7, 0);  // CTA start
+    if constexpr (kTrace) args.trace[((int64_t)blockIdx.x * 8 + 7) * 8 + 2] = (int64_t)clock64();
   }
   // Programmatic dependent launch: let the next kernel in the stream start
   // its CTAs (they wait in griddepcontrol.wait until this grid completes).
@@ -452,22 +563,22 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     }
     // A^T may be produced by the previous kernel in the stream (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const bool traced = args.trace != nullptr;
+    constexpr bool traced = kTrace;
     // (tracing) which producer thread records per-stage cycles: warp 0 (it
     // also issues the weight TMA) or, with debug bit 65536, warp 1
-    const int tr_thread = (args.debug & 65536) ? 32 : 0;
+    const int tr_thread = dbg<kTrace>(args, 65536) ? 32 : 0;
     for (int i = 0; i < n_st; ++i) {
       const int32_t *slot = ring + (i % kIdxSlots) * kSlotInts;
       const long long c0 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       // 4096 (experiment, needs 4 = no MMA): no back-pressure from the consumer
-      if (!(args.debug & 4096)) ptx::mbar_wait(&empty[stage], phase ^ 1);
+      if (!dbg<kTrace>(args, 4096)) ptx::mbar_wait(&empty[stage], phase ^ 1);
       const long long c1 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       // stage i's indices were the (kIdxLook)-th most recent group
       ptx::cp_async_wait_group<kIdxLook - 1>();
       __syncwarp();
       const long long c2 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       const int4 rec = *reinterpret_cast<const int4 *>(slot + kRowsPerWarp);
-      if (threadIdx.x == 0 && (rec.w & (1 << 16))) trace_evt(args, rec.w & 0xffff, 0);
+      if (threadIdx.x == 0 && (rec.w & (1 << 16))) trace_evt<kTrace>(args, rec.w & 0xffff, 0);
       const int nq = rec.z & 0xf;           // 64-token quarters in this unit
       const bool active = chunk < nq * 8;   // this lane's 8 tokens are in the unit
       const int mcol = rec.y + chunk * 8;
@@ -475,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
           !active ? 0u : (mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u));
       const char *lane_base = at_bytes + (src_bytes_m ? (int64_t)mcol * 2 : 0);
       if (warp == 0 && lane == 0) {
-        if (args.debug & 64) {  // experiment: no weight copy
+        if (dbg<kTrace>(args, 64)) {  // experiment: no weight copy
           ptx::mbar_arrive(&full[stage]);
         } else {
           ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes);
@@ -491,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         const int4 r4 = reinterpret_cast<const int4 *>(slot)[v4];
         rows[4 * v4] = r4.x; rows[4 * v4 + 1] = r4.y; rows[4 * v4 + 2] = r4.z; rows[4 * v4 + 3] = r4.w;
       }
-      if (args.debug & 8192) {  // experiment: synthetic rows (random, in range) instead of the kept lists
+      if (dbg<kTrace>(args, 8192)) {  // experiment: synthetic rows (random, in range) instead of the kept lists
 #pragma unroll
         for (int r = 0; r < kRowsPerWarp; ++r) rows[r] = ((warp * kRowsPerWarp + r) * 389 + i * 13 + blockIdx.x * 7) % 768;
       }
@@ -501,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       int min_row = rows[0];
 #pragma unroll
       for (int r = 1; r < kRowsPerWarp; ++r) min_row = min(min_row, rows[r]);
-      const bool fast = min_row >= 0 && rec.y + nq * 64 <= args.M && !(args.debug & 256);
+      const bool fast = min_row >= 0 && rec.y + nq * 64 <= args.M && !dbg<kTrace>(args, 256);
       // (tracing) the row indices and the record are in registers here
       const long long c2b = traced ? clock64() + (min_row & 0) : 0;
       // Units narrower than 256 tokens: R = 4 / nq rows per instruction
@@ -522,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
           ptx::cp_async_16_full(aw + rl * 128 + ((cq ^ (rl & 7)) * 16), lb + (int64_t)row * pitch);
         }
       };
-      const bool narrow = fast && nq * 8 < kChunks && (nq == 1 || nq == 2) && !(args.debug & 512);
+      const bool narrow = fast && nq * 8 < kChunks && (nq == 1 || nq == 2) && !dbg<kTrace>(args, 512);
       if (narrow && nq == 2) {
         gather_rows(std::integral_constant<int, 2>{});
       } else if (narrow) {
@@ -551,15 +662,15 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (i + kIdxLook < n_st) prefetch(i + kIdxLook);
       ptx::cp_async_mbar_arrive_noinc(&full[stage]);  // also covers the prefetch
       ptx::cp_async_commit();
-      if (threadIdx.x == 0) trace_stage(args, i, 0);
-      if (threadIdx.x == tr_thread && args.trace != nullptr && i < 32) {
+      if (threadIdx.x == 0) trace_stage<kTrace>(args, i, 0);
+      if (kTrace && threadIdx.x == tr_thread && i < 32) {
         const long long c3 = clock64();
         // 4 x 16 bits: wait_empty, wait_idx, index smem loads, issue
         args.trace[(int64_t)gridDim.x * 64 + ((int64_t)blockIdx.x * 32 + i) * 4 + 3] =
             (min(c1 - c0, 0xffffLL) << 48) | (min(c2 - c1, 0xffffLL) << 32) | (min(c2b - c2, 0xffffLL) << 16) |
             min(c3 - c2b, 0xffffLL);
       }
-      if (threadIdx.x == 0 && (rec.w & (1 << 17))) trace_evt(args, rec.w & 0xffff, 1);
+      if (threadIdx.x == 0 && (rec.w & (1 << 17))) trace_evt<kTrace>(args, rec.w & 0xffff, 1);
       if (++stage == C::kStages) { stage = 0; phase ^= 1; }
     }
     ptx::cp_async_wait_group<0>();
@@ -577,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       // full[stage] includes producer warp 0's cp.async arrival for stage i,
       // which covers its prefetch of stage i's record into its ring
       ptx::mbar_wait(&full[stage], phase);
-      if (lane == 0) trace_stage(args, i, 1);
+      if (lane == 0) trace_stage<kTrace>(args, i, 1);
       const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kIdxSlots) * kSlotInts + kRowsPerWarp);
       const int nq = rec.z & 0xf, nk = (rec.z >> 4) & 0xf;
       const uint32_t n_tok = (uint32_t)nq * 64u;  // MMA N = the unit's tokens
@@ -587,9 +698,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         d_tmem = tmem_base + (uint32_t)(acc * C::kAccCols);
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        if (lane == 0) trace_evt(args, rec.w & 0xffff, 2);
+        if (lane == 0) trace_evt<kTrace>(args, rec.w & 0xffff, 2);
       }
-      if (!(args.debug & 8)) ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
+      if (!dbg<kTrace>(args, 8)) ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
         // D[tile column][token] += W[column][k] * A^T[k][token]: the weight
@@ -601,20 +712,20 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 #pragma unroll
           for (int r = 0; r < BN / 128; ++r) {
             const uint64_t adesc = ptx::make_sw128_desc(b_base + stage * C::kBBytes + r * 16384 + kk * 32, 16, 1024);
-            if (!(args.debug & 4))
+            if (!dbg<kTrace>(args, 4))
               ptx::mma_f16_ss(d_tmem + r * 128, adesc, bdesc, idesc, (first && kk == 0) ? 0u : 1u);
           }
         }
-        if (args.debug & 16384) ptx::mbar_arrive(&empty[stage]);  // experiment (with 4): plain arrive, no commit
+        if (dbg<kTrace>(args, 16384)) ptx::mbar_arrive(&empty[stage]);  // experiment (with 4): plain arrive, no commit
         else ptx::mma_commit(&empty[stage]);
       }
       __syncwarp();
-      if (lane == 0) trace_stage(args, i, 2);
+      if (lane == 0) trace_stage<kTrace>(args, i, 2);
       if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       if (last) {
         if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
         __syncwarp();
-        if (lane == 0) trace_evt(args, rec.w & 0xffff, 3);
+        if (lane == 0) trace_evt<kTrace>(args, rec.w & 0xffff, 3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -630,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int q = warp & 3;
     const int h = e >> 2;
     const bool vec = ((args.ldc * (int64_t)sizeof(OutT)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
-    const bool bulk_ok = vec && ((int64_t)args.M * (int64_t)sizeof(OutT)) % 16 == 0 && !(args.debug & 32);
+    const bool bulk_ok = vec && ((int64_t)args.M * (int64_t)sizeof(OutT)) % 16 == 0 && !dbg<kTrace>(args, 32);
     // zero rows of this CTA: warp e writes rows z0+e, z0+e+8, ... (8 KB TMA
     // bulk stores) while it waits for an accumulator (policy 0: any unit; 1:
     // the CTA's last unit only; 2: none), and the rest at the end
@@ -643,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     volatile int32_t *s_zdone = reinterpret_cast<volatile int32_t *>(tmem_holder + 1);
     // the output may be read / written by the previous kernel (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int z1 = (args.accumulate || args.keep_pruned || (args.debug & 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
+    const int z1 = (args.accumulate || args.keep_pruned || dbg<kTrace>(args, 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
     int acc = 0;
     uint32_t acc_phase = 0;
     OutT *out = reinterpret_cast<OutT *>(args.out);
@@ -655,14 +766,14 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       // unit's table while others still store this unit's last chunk
       int32_t *ucol = sCol + ((j - u_begin) & 1) * BN;
       if (et < BN) ucol[et] = et < t.n_i ? __ldg(args.colids + t.col_off + et) : -1;
-      if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 4);
+      if (e == 0 && lane == 0) trace_evt<kTrace>(args, j - u_begin, 4);
       // wait for the accumulator, writing zero rows meanwhile
       // (non-blocking test_wait while there is filler work: try_wait would
       // suspend the warp for up to its time limit between zero rows)
       const bool fill = args.zero_policy == 0 || (args.zero_policy == 1 && j == u_end - 1);
       while (e == 0 && fill && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], acc_phase)) {
         if (lane == 0 && bulk_ok) {
-          if (args.debug & 2048) ptx::bulk_wait_read<2>(); else ptx::bulk_wait_read<0>();
+          if (dbg<kTrace>(args, 2048)) ptx::bulk_wait_read<2>(); else ptx::bulk_wait_read<0>();
         }
         zero_row_bulk<OutT, kPeer>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
         ++zr;
@@ -670,18 +781,23 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       epi_sync();  // sCol visible; previous unit's staging reads done
-      if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 5);
-      if (args.debug & 32768) {  // experiment: drop the accumulator unread
+      if (e == 0 && lane == 0) trace_evt<kTrace>(args, j - u_begin, 5);
+      if (dbg<kTrace>(args, 32768)) {  // experiment: drop the accumulator unread
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
+      } else if (!kPeer && !args.accumulate && bulk_ok && !dbg<kTrace>(args, 131072)) {
+        // TMA bulk-store epilogue (bit 131072: force the LSU path, experiment)
+        drain_unit_bulk<BN, OutT>(args, out, reinterpret_cast<uint8_t *>(sStage),
+                                  tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t, m0, nq, ucol, q, h, e,
+                                  lane);
       } else if (args.accumulate || sizeof(OutT) == 4) {
-        drain_unit<BN, OutT, float, 32, kPeer>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
+        drain_unit<BN, OutT, float, 32, kPeer, kTrace>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
                                          m0, nq, ucol, q, h, e, lane, vec);
       } else if constexpr (sizeof(OutT) == 2) {
-        drain_unit<BN, OutT, OutT, 64, kPeer>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
+        drain_unit<BN, OutT, OutT, 64, kPeer, kTrace>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
                                         m0, nq, ucol, q, h, e, lane, vec);
       }
-      if (e == 0 && lane == 0) trace_evt(args, j - u_begin, 6);
+      if (e == 0 && lane == 0) trace_evt<kTrace>(args, j - u_begin, 6);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -691,8 +807,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       zero_row_bulk<OutT, kPeer>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
     if (lane == 0) ptx::bulk_wait<0>();  // bulk stores performed (and smem read) before exit
     if (e == 0 && lane == 0) {
-      trace_evt(args, 7, 1);  // last zero row issued
-      if (args.trace != nullptr) args.trace[((int64_t)blockIdx.x * 8 + 7) * 8 + 3] = (int64_t)clock64();
+      trace_evt<kTrace>(args, 7, 1);  // last zero row issued
+      if constexpr (kTrace) args.trace[((int64_t)blockIdx.x * 8 + 7) * 8 + 3] = (int64_t)clock64();
     }
   }
 
@@ -703,9 +819,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   }
 }
 
-template <int BN, typename OutT, bool kPeer>
+template <int BN, typename OutT, bool kPeer, bool kTrace>
 cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
-  auto kern = tw_gemm_sm100_kernel<BN, OutT, kPeer>;
+  auto kern = tw_gemm_sm100_kernel<BN, OutT, kPeer, kTrace>;
   const int smem = (int)Cfg<BN>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -733,12 +849,17 @@ cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
 template <typename OutT>
 cudaError_t launch_out(const GemmArgs &args, int grid, cudaStream_t stream) {
   // peer-store variant (tw_gemm_peers) only when there are replicas: the
-  // extra store loop costs the plain kernel registers and ~1 us at C2a
+  // extra store loop costs the plain kernel registers and ~1 us at C2a;
+  // the traced variant (timeline stamps + experiment knobs) only for
+  // tw_gemm_traced -- the production instantiation carries neither
   if (args.n_peer > 0)
-    return args.block_n <= 128 ? launch_bn<128, OutT, true>(args, grid, stream)
-                               : launch_bn<256, OutT, true>(args, grid, stream);
-  return args.block_n <= 128 ? launch_bn<128, OutT, false>(args, grid, stream)
-                             : launch_bn<256, OutT, false>(args, grid, stream);
+    return args.block_n <= 128 ? launch_bn<128, OutT, true, false>(args, grid, stream)
+                               : launch_bn<256, OutT, true, false>(args, grid, stream);
+  if (args.trace != nullptr)
+    return args.block_n <= 128 ? launch_bn<128, OutT, false, true>(args, grid, stream)
+                               : launch_bn<256, OutT, false, true>(args, grid, stream);
+  return args.block_n <= 128 ? launch_bn<128, OutT, false, false>(args, grid, stream)
+                             : launch_bn<256, OutT, false, false>(args, grid, stream);
 }
 
 }  // namespace

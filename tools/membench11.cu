@@ -23,7 +23,7 @@
 #include <random>
 #include <vector>
 
-#include "tw_ptx.cuh"
+#include "tools_ptx.cuh"
 
 using namespace tw;
 

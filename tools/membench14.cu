@@ -20,7 +20,7 @@
 #include <random>
 #include <vector>
 
-#include "tw_ptx.cuh"
+#include "tools_ptx.cuh"
 
 using namespace tw;
 
@@ -88,8 +88,14 @@ __global__ void __launch_bounds__(1024, 1)
       if (warp < P) {
         // rows 0 .. 64-T-1: 16-byte cp.async, one row (256 tokens) per instruction
         const int blk = lane >> 3, cc = lane & 7;
-        for (int r = warp; r < 64 - T; r += P) {
-          const void *src = at + (int64_t)__ldg(krows + r) * g.M + tb * 256 + lane * 8;
+        constexpr int R = (64 - T) / P;  // rows per warp: all indices first, then the copies
+        int rows[R];
+#pragma unroll
+        for (int it = 0; it < R; ++it) rows[it] = __ldg(krows + warp * R + it);
+#pragma unroll
+        for (int it = 0; it < R; ++it) {
+          const int r = warp * R + it;
+          const void *src = at + (int64_t)rows[it] * g.M + tb * 256 + lane * 8;
           ptx::cp_async_16_full(sA + stage * kA + blk * 8192 + r * 128 + ((cc ^ (r & 7)) * 16), src);
         }
         ptx::cp_async_mbar_arrive_noinc(&full[stage]);
