@@ -35,8 +35,9 @@
 // accumulate, peer-store and unaligned cases use the LSU path (drain_unit:
 // staging read back, 16-byte streaming stores).
 //
-// Warp roles (416 threads): w0-3 producer (A gather + W bulk copy), w4 MMA
-// issuer + TMEM owner, w5-12 epilogue (TMEM lane quadrant = warp % 4).
+// Warp roles (448 threads): w0-3 producer (A gather), w4 MMA issuer + TMEM
+// owner, w5-12 epilogue (TMEM lane quadrant = warp % 4), w13 weight-block
+// TMA copies.
 #include <cuda.h>
 #include <cstdlib>
 #include <type_traits>
@@ -61,7 +62,11 @@ constexpr int kMmaWarp = kProducerWarps;
 constexpr int kEpiWarp0 = kProducerWarps + 1;
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kThreads = (kProducerWarps + 1 + kEpiWarps) * 32;
+// One more warp issues the per-stage weight-block TMA copies, so no gather
+// warp carries the expect_tx / bulk-copy issue (and its wait for the stage
+// record) on its per-stage critical path.
+constexpr int kWWarp = kEpiWarp0 + kEpiWarps;
+constexpr int kThreads = (kProducerWarps + 1 + kEpiWarps + 1) * 32;
 constexpr int kBlockK = 64;
 constexpr int kEpiBarrier = 1;  // named barrier id for the epilogue warps
 // Per-CTA stage stream (HostSchedule::stream): 64 kept-row indices + a
@@ -543,7 +548,6 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int chunk = lane % kChunks;
     const int rsub = lane / kChunks;
     const int blk = chunk >> 3, cc = chunk & 7;  // 64-token block, 16 B chunk in the 128 B row
-    const uint64_t keep = ptx::policy_evict_last();
     const char *at_bytes = reinterpret_cast<const char *>(args.at);
     const int64_t pitch = args.lda * 2;
     int stage = 0;
@@ -571,7 +575,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       const int32_t *slot = ring + (i % kIdxSlots) * kSlotInts;
       const long long c0 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       // 4096 (experiment, needs 4 = no MMA): no back-pressure from the consumer
-      if (!dbg<kTrace>(args, 4096)) ptx::mbar_wait(&empty[stage], phase ^ 1);
+      // the first kStages slots start free: skip the (already complete) wait
+      if (i >= C::kStages && !dbg<kTrace>(args, 4096)) ptx::mbar_wait(&empty[stage], phase ^ 1);
       const long long c1 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       // stage i's indices were the (kIdxLook)-th most recent group
       ptx::cp_async_wait_group<kIdxLook - 1>();
@@ -585,14 +590,6 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       const uint32_t src_bytes_m =
           !active ? 0u : (mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u));
       const char *lane_base = at_bytes + (src_bytes_m ? (int64_t)mcol * 2 : 0);
-      if (warp == 0 && lane == 0) {
-        if (dbg<kTrace>(args, 64)) {  // experiment: no weight copy
-          ptx::mbar_arrive(&full[stage]);
-        } else {
-          ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes);
-          ptx::bulk_g2s(sB + stage * C::kBBytes, args.wimg + rec.x, (uint32_t)args.wbytes, &full[stage], keep);
-        }
-      }
       uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + warp * kRowsPerWarp * 128;
       // all 16 row indices into registers BEFORE the first cp.async: a shared
       // load issued after a cp.async waits for it in the same (MIO) pipe
@@ -728,6 +725,32 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         if (lane == 0) trace_evt<kTrace>(args, rec.w & 0xffff, 3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp == kWWarp) {
+    // ------------------------------------------------ weight-block copies
+    // Stage i's weight block (one 1-D TMA bulk copy of wbytes) into stage
+    // slot i % kStages once the MMA has released the slot; the byte count
+    // rides on the stage's full barrier.  Weight offsets of 32 stages at a
+    // time are fetched lane-parallel from the stage stream and broadcast.
+    const uint64_t keep = ptx::policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i0 = 0; i0 < n_st; i0 += 32) {
+      const int mine = i0 + lane < n_st ? __ldg(args.stream + (int64_t)(s_begin + i0 + lane) * kIdxInts + 64) : 0;
+      const int cnt = min(32, n_st - i0);
+      for (int j = 0; j < cnt; ++j) {
+        const int woff = __shfl_sync(0xffffffffu, mine, j);
+        if (lane == 0) {
+          if (i0 + j >= C::kStages) ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (dbg<kTrace>(args, 64)) {  // experiment: no weight copy
+            ptx::mbar_arrive(&full[stage]);
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes);
+            ptx::bulk_g2s(sB + stage * C::kBBytes, args.wimg + woff, (uint32_t)args.wbytes, &full[stage], keep);
+          }
+        }
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
     }
   } else {
