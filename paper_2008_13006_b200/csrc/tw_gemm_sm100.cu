@@ -387,7 +387,7 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
   constexpr int kStride = kRowBytes + 16;
   constexpr int kPassTok = kRowBytes / (int)sizeof(OutT);
   constexpr int kWarpTok = BN <= 128 ? kPassTok / 2 : kPassTok;  // tokens per warp per pass
-  constexpr int kLoads = kWarpTok / 32;
+  constexpr int kLoads = kWarpTok / 32;  // at most; fewer for short units
   constexpr int kChunks = 32 * (int)sizeof(OutT) / 16;             // 16-byte chunks per 32 tokens
   static_assert(kRows * kStride <= 69632, "staging");
   const int toks = nq * 64;
@@ -395,7 +395,6 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
   const int region = BN <= 128 ? 0 : h;
   const int row = region * 128 + q * 32 + lane;  // staged row = tile column of this thread
   const bool warp_live = region * 128 + q * 32 < t.n_i;
-  const int tw0 = BN <= 128 ? h * kWarpTok : 0;
   const uint32_t t_base = t_acc + ((uint32_t)(q * 32) << 16) + (uint32_t)(region * 128);
   float bz = 0.f;
   if (args.bias != nullptr && row < t.n_i) bz = __ldg(args.bias + ucol[row]);
@@ -404,11 +403,17 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
     if (lane == 0) ptx::bulk_wait_read<0>();  // earlier bulk stores are done reading the staging rows
     epi_sync();
     const int ptok0 = p * kPassTok;
+    // BN <= 128: the warp pair (q, 0) / (q, 1) splits the pass's tokens in
+    // halves (multiples of 32: units are whole 64-token quarters), so short
+    // units keep all 8 warps loading TMEM
+    const int pt = min(kPassTok, toks - ptok0);
+    const int tw0 = BN <= 128 ? h * (pt / 2) : 0;
+    const int tw1 = BN <= 128 ? tw0 + pt / 2 : pt;
     if (warp_live) {
 #pragma unroll
       for (int x = 0; x < kLoads; ++x) {
         const int tau = ptok0 + tw0 + 32 * x;  // token (within the unit)
-        if (tau >= toks) break;                // warp-uniform
+        if (tw0 + 32 * x >= tw1) break;        // warp-uniform
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)tau, v);
         ptx::tmem_ld_wait();
@@ -828,7 +833,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     epi_sync();
     for (zr = *s_zdone + e; zr < z1; zr += kEpiWarps)
       zero_row_bulk<OutT, kPeer>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
-    if (lane == 0) ptx::bulk_wait<0>();  // bulk stores performed (and smem read) before exit
+    // before exit the bulk stores must have READ shared memory (it is
+    // released with the CTA); their global writes complete with the grid
+    // (the same contract as CUTLASS's TMA-store epilogues)
+    if (lane == 0) ptx::bulk_wait_read<0>();
     if (e == 0 && lane == 0) {
       trace_evt<kTrace>(args, 7, 1);  // last zero row issued
       if constexpr (kTrace) args.trace[((int64_t)blockIdx.x * 8 + 7) * 8 + 3] = (int64_t)clock64();
