@@ -679,57 +679,67 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------ MMA issuer
     // Walks the same stage stream (records from the shared index ring).
-    int stage = 0;
+    // Each stage accumulates into the TMEM region its record names (a piece
+    // of two halves keeps both regions live, its stages interleaved); a
+    // stage flagged "W from the previous stage" reads the previous stage's
+    // weight block, which therefore releases its slot only after this
+    // stage's MMAs (the deferred commit below).
+    int stage = 0, prev_stage = 0;
     uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t use[2] = {0, 0};  // completed uses of each accumulator region
     const uint32_t a_base = ptx::smem_u32(sA);
     const uint32_t b_base = ptx::smem_u32(sB);
-    uint32_t d_tmem = tmem_base;
     for (int i = 0; i < n_st; ++i) {
       // full[stage] includes producer warp 0's cp.async arrival for stage i,
       // which covers its prefetch of stage i's record into its ring
       ptx::mbar_wait(&full[stage], phase);
       if (lane == 0) trace_stage<kTrace>(args, i, 1);
       const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kIdxSlots) * kSlotInts + kRowsPerWarp);
-      const int nq = rec.z & 0xf, nk = (rec.z >> 4) & 0xf;
-      const uint32_t n_tok = (uint32_t)nq * 64u;  // MMA N = the unit's tokens
+      const int nq = rec.z & 0xf, nk = (rec.z >> 4) & 0xf, region = (rec.z >> 8) & 1;
+      const bool w_prev = (rec.z >> 9) & 1, defer = (rec.z >> 10) & 1;
+      const uint32_t n_tok = (uint32_t)nq * 64u;  // MMA N = the half's tokens
       const uint32_t idesc = args.idesc | ((n_tok >> 3) << 17);
       const bool first = rec.w & (1 << 16), last = rec.w & (1 << 17);
-      if (first) {
-        d_tmem = tmem_base + (uint32_t)(acc * C::kAccCols);
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      const uint32_t d_tmem = tmem_base + (uint32_t)(region * C::kAccCols);
+      if (first) {  // the epilogue has drained this region's previous half
+        ptx::mbar_wait(&tempty[region], (use[region] & 1) ^ 1);
         ptx::tc_fence_after();
         if (lane == 0) trace_evt<kTrace>(args, rec.w & 0xffff, 2);
       }
       if (!dbg<kTrace>(args, 8)) ptx::fence_proxy_async_smem();  // cp.async data was written through the generic proxy
       ptx::tc_fence_after();
+      const int wslot = w_prev ? prev_stage : stage;
       if (ptx::elect_one()) {
         // D[tile column][token] += W[column][k] * A^T[k][token]: the weight
         // block is the K-major A operand (M = 128 columns), the gathered A^T
-        // rows the MN-major B operand (N = the unit's tokens, 64-token SW128
+        // rows the MN-major B operand (N = the half's tokens, 64-token SW128
         // blocks 8 KB apart)
         for (int kk = 0; kk < nk; ++kk) {
           const uint64_t bdesc = ptx::make_sw128_desc(a_base + stage * C::kABytes + kk * 2048, 8192, 1024);
 #pragma unroll
           for (int r = 0; r < BN / 128; ++r) {
-            const uint64_t adesc = ptx::make_sw128_desc(b_base + stage * C::kBBytes + r * 16384 + kk * 32, 16, 1024);
+            const uint64_t adesc = ptx::make_sw128_desc(b_base + wslot * C::kBBytes + r * 16384 + kk * 32, 16, 1024);
             if (!dbg<kTrace>(args, 4))
               ptx::mma_f16_ss(d_tmem + r * 128, adesc, bdesc, idesc, (first && kk == 0) ? 0u : 1u);
           }
         }
-        if (dbg<kTrace>(args, 16384)) ptx::mbar_arrive(&empty[stage]);  // experiment (with 4): plain arrive, no commit
-        else ptx::mma_commit(&empty[stage]);
+        if (dbg<kTrace>(args, 16384)) {  // experiment (with 4): plain arrive, no commit
+          if (!defer) ptx::mbar_arrive(&empty[stage]);
+          if (w_prev) ptx::mbar_arrive(&empty[prev_stage]);
+        } else {
+          if (w_prev) ptx::mma_commit(&empty[prev_stage]);  // its weight block is no longer read
+          if (!defer) ptx::mma_commit(&empty[stage]);
+        }
       }
       __syncwarp();
       if (lane == 0) trace_stage<kTrace>(args, i, 2);
+      prev_stage = stage;
       if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       if (last) {
-        if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
+        if (ptx::elect_one()) ptx::mma_commit(&tfull[region]);
         __syncwarp();
         if (lane == 0) trace_evt<kTrace>(args, rec.w & 0xffff, 3);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        ++use[region];
       }
     }
   } else if (warp == kWWarp) {
@@ -748,7 +758,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         const int woff = __shfl_sync(0xffffffffu, mine, j);
         if (lane == 0) {
           if (i0 + j >= C::kStages) ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (dbg<kTrace>(args, 64)) {  // experiment: no weight copy
+          if (woff < 0 || dbg<kTrace>(args, 64)) {  // reuses the previous stage's block (or experiment: no copy)
             ptx::mbar_arrive(&full[stage]);
           } else {
             ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes);
@@ -783,13 +793,15 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // the output may be read / written by the previous kernel (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int z1 = (args.accumulate || args.keep_pruned || dbg<kTrace>(args, 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
-    int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t use[2] = {0, 0};  // drained halves per accumulator region
     OutT *out = reinterpret_cast<OutT *>(args.out);
     for (int j = u_begin; j < u_end; ++j) {
+      // one epilogue unit per accumulator half, in completion order:
+      // {live tile, first token, quarters, TMEM region}
       const int4 su = __ldg(args.sched + j);
       const TileMeta t = args.tiles[su.x];
-      const int m0 = su.y, nq = su.z;
+      const int m0 = su.y, nq = su.z, acc = su.w & 1;
+      const uint32_t acc_phase = use[acc] & 1;
       // col ids double-buffered by unit parity: a fast warp may fill the next
       // unit's table while others still store this unit's last chunk
       int32_t *ucol = sCol + ((j - u_begin) & 1) * BN;
@@ -826,8 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
                                         m0, nq, ucol, q, h, e, lane, vec);
       }
       if (e == 0 && lane == 0) trace_evt<kTrace>(args, j - u_begin, 6);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      ++use[acc];
     }
     if (e == 0 && lane == 0) *s_zdone = zr;
     epi_sync();

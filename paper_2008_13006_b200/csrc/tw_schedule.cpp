@@ -9,13 +9,15 @@
 // roofline of this kernel at high sparsity, so every CTA should
 // write the same number of bytes.
 //
-// Unit cost model (ns per CTA-SM, calibrated on B200 with tools/membench*.cu):
+// Piece cost model (ns per CTA-SM, calibrated on B200 with tools/membench*.cu):
 // output bytes at ~30 B/ns per SM (4.5 TB/s DRAM write over 148 SMs), gathered
 // input bytes at ~90 B/ns (L2 -> SM), MMA at 8192 flop/clk, plus a fixed
-// pipeline fill.  Tail units of 256 tokens may be split into two 128-token
-// units when that shortens the makespan (wave quantization).
+// pipeline fill and a per-stage producer overhead.  Every tile's token range
+// is cut into equal pieces of at most P quarters for P = 1 .. 2 TB/64; the P
+// whose LPT makespan is shortest wins (wave quantization vs weight re-reads).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <numeric>
 #include <climits>
@@ -27,7 +29,11 @@ namespace tw {
 
 namespace {
 
-// nq = the unit's tokens in 64-token quarters (1..4; 1..2 for G = 256)
+// A piece = (live tile, first token, nq 64-token quarters).  Pieces of up to
+// TB tokens are one accumulator "half"; longer pieces (up to 2 TB) are two
+// halves sharing every weight block: the stage stream interleaves them per
+// 64-k block (h0, h1, h0, h1, ...), the h1 stage reads the weight block the
+// h0 stage loaded, so the tile's weights cross L2 -> SM once per 2 TB tokens.
 struct Unit {
   int32_t tile, m0, nq;
   double cost;
@@ -37,13 +43,15 @@ constexpr double kWriteBps = 30.0;   // bytes / ns / SM
 constexpr double kReadBps = 90.0;    // bytes / ns / SM
 constexpr double kMmaFlops = 15000;  // flop / ns / SM (8192 flop/clk at ~1.85 GHz)
 constexpr double kFixedNs = 300.0;
+constexpr double kStageNs = 150.0;   // per-stage producer overhead (index loads, barriers)
 
-double unit_cost(const TileMeta &t, int nq, int ob) {
+double unit_cost(const TileMeta &t, int nq, int ob, int tb) {
   const double toks = 64.0 * nq;
   const double out_b = toks * t.n_i * ob;
-  const double in_b = (double)t.k_i * (toks * 2.0 + t.n_i * 2.0);
+  const double in_b = (double)t.k_i * (toks * 2.0 + t.n_i * 2.0);  // weights once per piece
   const double mma = 2.0 * toks * ((t.n_i + 15) / 16 * 16) * (t.k16 * 16.0) / kMmaFlops;
-  return std::max(std::max(out_b / kWriteBps, in_b / kReadBps), mma) + kFixedNs;
+  const int halves = nq * 64 > tb ? 2 : 1;
+  return std::max(std::max(out_b / kWriteBps, in_b / kReadBps), mma) + kFixedNs + kStageNs * t.nkb * halves;
 }
 
 // LPT: units (already sorted by cost, descending) to G workers; returns loads.
@@ -110,49 +118,66 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
   s = HostSchedule{};
   const int64_t Z = zero_rows ? (int64_t)hp.zero_rows.size() : 0;
   const double zc = (double)m * ob / kWriteBps;
-  std::vector<Unit> base;
-  for (int32_t t = 0; t < (int32_t)hp.tiles.size(); ++t) {
-    for (int64_t m0 = 0; m0 < m; m0 += tb) {
-      const int nq = (int)std::min<int64_t>(tb / 64, (m - m0 + 63) / 64);
-      base.push_back({t, (int32_t)m0, nq, unit_cost(hp.tiles[(size_t)t], nq, ob)});
-    }
-  }
-  const int64_t zero_ctas = Z > 0 ? (Z * m * ob + (256 << 10) - 1) / (256 << 10) : 0;
-  // CTAs: enough for every unit -- or every 64-token quarter, so small
-  // layers (fewer 256-token units than SMs) can spread over more SMs
-  int64_t quarters = 0;
-  for (const Unit &u : base) quarters += u.nq;
-  int G = (int)std::min<int64_t>(sms, std::max<int64_t>({quarters, zero_ctas, (int64_t)1}));
+  const int qmax = 2 * tb / 64;  // quarters per piece (two halves of tb tokens)
+  const int64_t q_tile = (m + 63) / 64;
   auto by_cost = [](const Unit &a, const Unit &b) {
     return a.cost != b.cost ? a.cost > b.cost : (a.tile != b.tile ? a.tile < b.tile : a.m0 < b.m0);
   };
-  std::stable_sort(base.begin(), base.end(), by_cost);
-
-  // Candidate unit sets: as is; the tail (units past the last whole wave)
-  // or everything split into pieces of at most 2 quarters, or of 1 quarter.
-  // A piece re-reads the tile's whole weight block, so smaller pieces only
-  // win where they shorten the makespan -- the cost model decides.
-  std::vector<std::vector<Unit>> cands{base};
-  auto split = [&](const std::vector<Unit> &from_set, size_t from, int max_nq) {
-    std::vector<Unit> u(from_set.begin(), from_set.begin() + (std::ptrdiff_t)from);
-    for (size_t i = from; i < from_set.size(); ++i) {
-      const Unit &b = from_set[i];
-      const TileMeta &t = hp.tiles[(size_t)b.tile];
-      for (int q = 0; q < b.nq; q += max_nq) {
-        const int nq = std::min(max_nq, b.nq - q);
-        u.push_back({b.tile, b.m0 + 64 * q, nq, unit_cost(t, nq, ob)});
+  // pieces of at most P quarters: every tile's quarter range cut into
+  // ceil(q / P) nearly equal contiguous pieces
+  auto pieces = [&](int P) {
+    std::vector<Unit> u;
+    for (int32_t t = 0; t < (int32_t)hp.tiles.size(); ++t) {
+      const int64_t np = (q_tile + P - 1) / P;
+      int64_t q0 = 0;
+      for (int64_t i = 0; i < np; ++i) {
+        const int64_t q1 = (q_tile * (i + 1)) / np;
+        const int nq = (int)(q1 - q0);
+        if (nq > 0) u.push_back({t, (int32_t)(q0 * 64), nq, unit_cost(hp.tiles[(size_t)t], nq, ob, tb)});
+        q0 = q1;
+      }
+    }
+    std::stable_sort(u.begin(), u.end(), by_cost);
+    return u;
+  };
+  const int64_t zero_ctas = Z > 0 ? (Z * m * ob + (256 << 10) - 1) / (256 << 10) : 0;
+  // CTAs: enough for every piece of one quarter, so small layers (fewer
+  // pieces than SMs) can spread over more SMs
+  const int64_t quarters = q_tile * (int64_t)hp.tiles.size();
+  int G = (int)std::min<int64_t>(sms, std::max<int64_t>({quarters, zero_ctas, (int64_t)1}));
+  // Candidates: whole units of tb tokens; the tail past the last full wave,
+  // or everything, split into pieces of P < tb/64 quarters; and (opt-in,
+  // TW_B200_PAIRS=1) two-half pieces sharing weight blocks.  Measured on
+  // B200: two-half pieces lose (C2a 12.5 -> 15.7 us) -- both TMEM regions
+  // stay live to the end of a piece, so its epilogue no longer overlaps the
+  // next piece's mainloop -- so they are off by default.
+  static const bool pairs = [] {
+    const char *e = std::getenv("TW_B200_PAIRS");
+    return e && e[0] == '1';
+  }();
+  const int qh = tb / 64;
+  std::vector<std::vector<Unit>> cands{pieces(qh)};
+  const std::vector<Unit> base = cands[0];  // a copy: cands grows below
+  auto split_tail = [&](size_t from, int P) {
+    std::vector<Unit> u(base.begin(), base.begin() + (std::ptrdiff_t)from);
+    for (size_t i = from; i < base.size(); ++i) {
+      const Unit &b = base[i];
+      for (int q = 0; q < b.nq; q += P) {
+        const int nq = std::min(P, b.nq - q);
+        u.push_back({b.tile, b.m0 + 64 * q, nq, unit_cost(hp.tiles[(size_t)b.tile], nq, ob, tb)});
       }
     }
     std::stable_sort(u.begin(), u.end(), by_cost);
     return u;
   };
   const size_t full = base.size() / (size_t)G * (size_t)G;
-  for (int max_nq : {2, 1}) {
-    if (max_nq >= tb / 64) continue;
-    if (full < base.size() && full > 0) cands.push_back(split(base, full, max_nq));
-    cands.push_back(split(base, 0, max_nq));
+  for (int P = 1; P < qh; ++P) {
+    if (full < base.size() && full > 0) cands.push_back(split_tail(full, P));
+    cands.push_back(pieces(P));
   }
-  // Pick the candidate with the shortest unit-only makespan (a CTA's units
+  if (pairs)
+    for (int P = qh + 1; P <= qmax; ++P) cands.push_back(pieces(P));
+  // Pick the candidate with the shortest piece-only makespan (a CTA's pieces
   // run back to back and their outputs cannot be written before their MMA
   // completes); the zero rows are then water-filled around it.
   double best = 1e300, best_total = 0;
@@ -160,12 +185,13 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
   std::vector<int> best_owner;
   std::vector<int64_t> best_z;
   for (size_t ci = 0; ci < cands.size(); ++ci) {
+    if (cands[ci].empty() && ci > 0) continue;
     std::vector<int> owner;
     std::vector<double> load = lpt(cands[ci], G, &owner);
     const double unit_mk = *std::max_element(load.begin(), load.end());
     double mk = 0;
     std::vector<int64_t> z = water_fill(load, Z, zc, &mk);
-    if (unit_mk < best * 0.98 || (unit_mk < best * 1.02 && mk < best_total)) {
+    if (unit_mk < best * 0.99 || (unit_mk < best * 1.01 && mk < best_total)) {
       best = unit_mk;
       best_total = mk;
       best_i = ci;
@@ -174,52 +200,59 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
     }
   }
   const std::vector<Unit> &units = cands[best_i];
-  // emit per-CTA lists (units keep their global cost order within a CTA)
+  // per-CTA piece lists (pieces keep their global cost order within a CTA:
+  // the smallest last, for the shortest epilogue tail)
   std::vector<std::vector<int>> per((size_t)G);
   for (size_t i = 0; i < units.size(); ++i) per[(size_t)best_owner[i]].push_back((int)i);
   s.grid = G;
   s.off.assign((size_t)G + 1, 0);
   s.zoff.assign((size_t)G + 1, 0);
-  double total = 0;
-  for (int c = 0; c < G; ++c) {
-    for (int i : per[(size_t)c]) {
-      const Unit &u = units[(size_t)i];
-      s.units.insert(s.units.end(), {u.tile, u.m0, u.nq, 0});
-      total += u.cost;
-    }
-    s.off[(size_t)c + 1] = (int32_t)(s.units.size() / 4);
-    s.zoff[(size_t)c + 1] = (int32_t)(s.zoff[(size_t)c] + (best_z.empty() ? 0 : best_z[(size_t)c]));
-  }
-  if (s.zoff[(size_t)G] != Z) return fail(TW_ERR_ARG, "internal: zero-row schedule does not cover the zero list");
-  // per-CTA stage streams (see HostSchedule)
-  const int64_t wbytes = (int64_t)hp.wrows * 128;
   s.soff.assign((size_t)G + 1, 0);
+  const int64_t wbytes = (int64_t)hp.wrows * 128;
+  double total = 0;
   int64_t n_stages = 0;
   for (int c = 0; c < G; ++c) {
-    for (int32_t u = s.off[(size_t)c]; u < s.off[(size_t)c + 1]; ++u) {
-      const int32_t *un = &s.units[(size_t)u * 4];
-      const TileMeta &t = hp.tiles[(size_t)un[0]];
-      const int32_t n_mma = (t.n_i + 15) & ~15;
+    int half_no = 0;  // accumulator region of a half = its ordinal in the CTA, mod 2
+    for (int i : per[(size_t)c]) {
+      const Unit &u = units[(size_t)i];
+      total += u.cost;
+      const TileMeta &t = hp.tiles[(size_t)u.tile];
+      const bool pair = u.nq > qh;
+      const int nh = pair ? 2 : 1;
+      int hq[2] = {pair ? qh : u.nq, pair ? u.nq - qh : 0};
+      int hm0[2] = {u.m0, u.m0 + qh * 64};
+      int reg[2] = {half_no & 1, (half_no + 1) & 1};
+      // epilogue units: one per half, in completion order
+      for (int h = 0; h < nh; ++h) s.units.insert(s.units.end(), {u.tile, hm0[h], hq[h], reg[h]});
       for (int kb = 0; kb < t.nkb; ++kb) {
-        for (int r = 0; r < 64; ++r) {
-          const int32_t idx = hp.kidx[(size_t)t.kidx_off + (size_t)kb * 64 + (size_t)r];
-          s.stream.push_back(kb * 64 + r < t.k_i && idx < hp.a_rows ? idx : -1);
-        }
         const int64_t woff = t.w_off + kb * wbytes;
         if (woff > INT32_MAX) return fail(TW_ERR_UNSUPPORTED, "weight image larger than 2 GiB");
         const int32_t nk = std::min(4, t.k16 - kb * 4);
-        s.stream.insert(s.stream.end(),
-                        {(int32_t)woff, un[1], un[2] | (nk << 4) | (n_mma << 8),
-                         // unit ordinal (tracing only) masked to 16 bits: bits 16/17 are
-                         // the first/last-block flags the MMA warp acts on
-                         ((u - s.off[(size_t)c]) & 0xffff) | (kb == 0 ? 1 << 16 : 0) |
-                             (kb == t.nkb - 1 ? 1 << 17 : 0)});
-        ++n_stages;
+        for (int h = 0; h < nh; ++h) {
+          for (int r = 0; r < 64; ++r) {
+            const int32_t idx = hp.kidx[(size_t)t.kidx_off + (size_t)kb * 64 + (size_t)r];
+            s.stream.push_back(kb * 64 + r < t.k_i && idx < hp.a_rows ? idx : -1);
+          }
+          // record: {weight block offset (-1: reuse the previous stage's),
+          //          first token, quarters | k-steps << 4 | region << 8 |
+          //          W from the previous stage << 9 | defer the slot release << 10,
+          //          half ordinal (tracing, 16 bits) | first << 16 | last << 17}
+          const int32_t flags = hq[h] | (nk << 4) | (reg[h] << 8) | (h == 1 ? 1 << 9 : 0) |
+                                (pair && h == 0 ? 1 << 10 : 0);
+          s.stream.insert(s.stream.end(),
+                          {h == 0 ? (int32_t)woff : -1, hm0[h], flags,
+                           ((half_no + h) & 0xffff) | (kb == 0 ? 1 << 16 : 0) | (kb == t.nkb - 1 ? 1 << 17 : 0)});
+          ++n_stages;
+        }
       }
+      half_no += nh;
     }
+    s.off[(size_t)c + 1] = (int32_t)(s.units.size() / 4);
+    s.zoff[(size_t)c + 1] = (int32_t)(s.zoff[(size_t)c] + (best_z.empty() ? 0 : best_z[(size_t)c]));
     if (n_stages > INT32_MAX / 68) return fail(TW_ERR_UNSUPPORTED, "schedule too long");
     s.soff[(size_t)c + 1] = (int32_t)n_stages;
   }
+  if (s.zoff[(size_t)G] != Z) return fail(TW_ERR_ARG, "internal: zero-row schedule does not cover the zero list");
   s.makespan_ns = best_total;
   s.mean_ns = (total + Z * zc) / G;
   return TW_OK;
