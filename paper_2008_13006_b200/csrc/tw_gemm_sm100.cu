@@ -35,9 +35,10 @@
 // accumulate, peer-store and unaligned cases use the LSU path (drain_unit:
 // staging read back, 16-byte streaming stores).
 //
-// Warp roles (448 threads): w0-3 producer (A gather), w4 MMA issuer + TMEM
-// owner, w5-12 epilogue (TMEM lane quadrant = warp % 4), w13 weight-block
-// TMA copies.
+// Warp roles (G = kProducerGroups, default 1: 448 threads): w0..4G-1
+// producer (A gather; G groups of 4 taking alternate stages), w4G MMA issuer
+// + TMEM owner, the next 8 epilogue (TMEM lane quadrant = warp % 4), the
+// last one the weight-block TMA copies.
 #include <cuda.h>
 #include <cstdlib>
 #include <type_traits>
@@ -52,11 +53,18 @@ namespace tw {
 
 namespace {
 
-#ifndef TW_PRODUCER_WARPS
-#define TW_PRODUCER_WARPS 4
+// Producer: kProducerGroups groups of kGroupWarps gather warps; group g
+// issues stages g, g + G, g + 2G, ...  A warp's per-stage chain -- its row
+// indices come from shared memory, and a shared load queues behind the
+// warp's own outstanding cp.async gathers -- is latency-bound; alternating
+// groups keep G stages of gathers in issue at once.
+#ifndef TW_PRODUCER_GROUPS
+#define TW_PRODUCER_GROUPS 1
 #endif
-constexpr int kProducerWarps = TW_PRODUCER_WARPS;
-constexpr int kRowsPerWarp = 64 / kProducerWarps;  // kept rows of a 64-k stage per producer warp
+constexpr int kProducerGroups = TW_PRODUCER_GROUPS;
+constexpr int kGroupWarps = 4;
+constexpr int kProducerWarps = kProducerGroups * kGroupWarps;
+constexpr int kRowsPerWarp = 64 / kGroupWarps;     // kept rows of a 64-k stage per producer warp
 constexpr int kIdxLanes = kRowsPerWarp / 4;        // lanes that prefetch this warp's row indices
 constexpr int kMmaWarp = kProducerWarps;
 constexpr int kEpiWarp0 = kProducerWarps + 1;
@@ -75,8 +83,8 @@ constexpr int kEpiBarrier = 1;  // named barrier id for the epilogue warps
 // cp.async while issuing stage i: no register ever waits on an index load.
 constexpr int kIdxInts = 68;
 constexpr int kSlotInts = kRowsPerWarp + 4;  // this warp's row indices + the 4-int record
-constexpr int kIdxSlots = 8;
-constexpr int kIdxLook = 4;
+constexpr int kIdxSlots = 6;  // per warp, in the warp's own stage numbering
+constexpr int kIdxLook = 3;
 
 template <int BN>
 struct Cfg {
@@ -378,10 +386,18 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
 //   BN <= 128: 128 rows x 512 B per pass (16-bit: the whole 256-token unit;
 //     fp32: 128 tokens); warp (q, h): rows 32q.., tokens h * pass/2 ..
 //   BN == 256: 256 rows x 256 B per pass; warp (q, h): rows 128h + 32q..
-template <int BN, typename OutT>
+// (tracing) SM-clock stamps of the bulk epilogue of a CTA's first unit:
+// trace[grid*192 + cta*32 + pass*4 + {0 staging free, 1 staged, 2 synced, 3 issued}]
+template <bool kTrace>
+__device__ __forceinline__ void trace_epi(const GemmArgs &a, int unit_i, int pass, int slot, int e, int lane) {
+  if (kTrace && unit_i == 0 && pass < 8 && e == 0 && lane == 0)
+    a.trace[(int64_t)gridDim.x * 192 + (int64_t)blockIdx.x * 32 + pass * 4 + slot] = (int64_t)clock64();
+}
+
+template <int BN, typename OutT, bool kTrace>
 __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out, uint8_t *sStg, uint32_t t_acc,
                                                 uint64_t *tempty, const TileMeta &t, int m0, int nq,
-                                                const int32_t *ucol, int q, int h, int e, int lane) {
+                                                const int32_t *ucol, int q, int h, int e, int lane, int unit_i) {
   constexpr int kRows = BN <= 128 ? 128 : 256;
   constexpr int kRowBytes = BN <= 128 ? 512 : 256;
   constexpr int kStride = kRowBytes + 16;
@@ -400,8 +416,10 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
   if (args.bias != nullptr && row < t.n_i) bz = __ldg(args.bias + ucol[row]);
   uint8_t *srow = sStg + row * kStride;
   for (int p = 0; p < n_pass; ++p) {
+    if (p == 0) trace_epi<kTrace>(args, unit_i, 7, 0, e, lane);  // (tracing) entry
     if (lane == 0) ptx::bulk_wait_read<0>();  // earlier bulk stores are done reading the staging rows
     epi_sync();
+    trace_epi<kTrace>(args, unit_i, p, 0, e, lane);
     const int ptok0 = p * kPassTok;
     // BN <= 128: the warp pair (q, 0) / (q, 1) splits the pass's tokens in
     // halves (multiples of 32: units are whole 64-token quarters), so short
@@ -435,8 +453,10 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty);
     }
+    trace_epi<kTrace>(args, unit_i, p, 1, e, lane);
     ptx::fence_proxy_async_smem();  // the staged rows are read by the TMA (async proxy)
     epi_sync();
+    trace_epi<kTrace>(args, unit_i, p, 2, e, lane);
     if (lane == 0) {
       const int tok_n = min(kPassTok, min(toks - ptok0, args.M - m0 - ptok0));
       if (tok_n > 0) {
@@ -450,6 +470,7 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
         ptx::bulk_commit();
       }
     }
+    trace_epi<kTrace>(args, unit_i, p, 3, e, lane);
   }
 }
 
@@ -523,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      ptx::mbar_init(&full[s], 1u + kProducerWarps * 32u);  // W bulk arrive(+tx) + one cp.async arrival per thread
+      ptx::mbar_init(&full[s], 1u + kGroupWarps * 32u);  // W bulk arrive(+tx) + one cp.async arrival per group thread
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -555,19 +576,20 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const int blk = chunk >> 3, cc = chunk & 7;  // 64-token block, 16 B chunk in the 128 B row
     const char *at_bytes = reinterpret_cast<const char *>(args.at);
     const int64_t pitch = args.lda * 2;
-    int stage = 0;
-    uint32_t phase = 0;
+    const int grp = warp / kGroupWarps, gw = warp % kGroupWarps;  // group, warp within the group
+    const int my_st = n_st > grp ? (n_st - grp + kProducerGroups - 1) / kProducerGroups : 0;  // this group's stages
     int32_t *ring = sIdx + warp * (kIdxSlots * kSlotInts);  // this warp's index ring
-    // stage k's 16 row indices of this warp (lanes 0-3) + record (lane 4)
+    // the group's k-th stage (global stage grp + k * G): this warp's 16 row
+    // indices (lanes 0-3) + the record (lane 4)
     auto prefetch = [&](int k) {
       if (lane <= kIdxLanes) {
-        const int32_t *src =
-            args.stream + (int64_t)(s_begin + k) * kIdxInts + (lane < kIdxLanes ? warp * kRowsPerWarp + lane * 4 : 64);
+        const int32_t *src = args.stream + (int64_t)(s_begin + grp + k * kProducerGroups) * kIdxInts +
+                             (lane < kIdxLanes ? gw * kRowsPerWarp + lane * 4 : 64);
         ptx::cp_async_16(ring + (k % kIdxSlots) * kSlotInts + lane * 4, src, 16);
       }
     };
     for (int k = 0; k < kIdxLook; ++k) {  // one cp.async group per prefetched stage
-      if (k < n_st) prefetch(k);
+      if (k < my_st) prefetch(k);
       ptx::cp_async_commit();
     }
     // A^T may be produced by the previous kernel in the stream (PDL)
@@ -576,8 +598,11 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // (tracing) which producer thread records per-stage cycles: warp 0 (it
     // also issues the weight TMA) or, with debug bit 65536, warp 1
     const int tr_thread = dbg<kTrace>(args, 65536) ? 32 : 0;
-    for (int i = 0; i < n_st; ++i) {
-      const int32_t *slot = ring + (i % kIdxSlots) * kSlotInts;
+    for (int li = 0; li < my_st; ++li) {
+      const int i = grp + li * kProducerGroups;  // global stage
+      const int stage = i % C::kStages;
+      const uint32_t phase = (uint32_t)(i / C::kStages) & 1u;
+      const int32_t *slot = ring + (li % kIdxSlots) * kSlotInts;
       const long long c0 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       // 4096 (experiment, needs 4 = no MMA): no back-pressure from the consumer
       // the first kStages slots start free: skip the (already complete) wait
@@ -595,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       const uint32_t src_bytes_m =
           !active ? 0u : (mcol + 8 <= args.M ? 16u : (mcol < args.M ? (uint32_t)(args.M - mcol) * 2u : 0u));
       const char *lane_base = at_bytes + (src_bytes_m ? (int64_t)mcol * 2 : 0);
-      uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + warp * kRowsPerWarp * 128;
+      uint8_t *a_warp = sA + stage * C::kABytes + blk * 8192 + gw * kRowsPerWarp * 128;
       // all 16 row indices into registers BEFORE the first cp.async: a shared
       // load issued after a cp.async waits for it in the same (MIO) pipe
       int rows[kRowsPerWarp];
@@ -606,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       }
       if (dbg<kTrace>(args, 8192)) {  // experiment: synthetic rows (random, in range) instead of the kept lists
 #pragma unroll
-        for (int r = 0; r < kRowsPerWarp; ++r) rows[r] = ((warp * kRowsPerWarp + r) * 389 + i * 13 + blockIdx.x * 7) % 768;
+        for (int r = 0; r < kRowsPerWarp; ++r) rows[r] = ((gw * kRowsPerWarp + r) * 389 + i * 13 + blockIdx.x * 7) % 768;
       }
       // Fast path (warp-uniform): every row real and the unit's full token
       // range inside M -> plain 16-byte cp.async.  The zero-fill form (with a
@@ -624,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         constexpr int L = 32 / R;               // 16-byte chunks (lanes) per row
         const int ch = lane % L, rs = lane / L, cq = ch & 7;
         const char *lb = at_bytes + (int64_t)(rec.y + ch * 8) * 2;
-        uint8_t *aw = sA + stage * C::kABytes + (ch >> 3) * 8192 + warp * kRowsPerWarp * 128;
+        uint8_t *aw = sA + stage * C::kABytes + (ch >> 3) * 8192 + gw * kRowsPerWarp * 128;
 #pragma unroll
         for (int it = 0; it < kRowsPerWarp / R; ++it) {
           const int rl = it * R + rs;
@@ -658,10 +683,11 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
                              nbytes ? lane_base + (int64_t)row * pitch : at_bytes, nbytes);
         }
       }
-      // Slot (i + kIdxLook) % kIdxSlots last held stage i + kIdxLook - kIdxSlots,
-      // which this warp has issued and the MMA warp has committed (we passed
-      // empty[i], so stage i - kStages is consumed): free to overwrite.
-      if (i + kIdxLook < n_st) prefetch(i + kIdxLook);
+      // Slot (li + kIdxLook) % kIdxSlots last held the group's stage
+      // li + kIdxLook - kIdxSlots (global i - G * (kIdxSlots - kIdxLook) <=
+      // i - kStages), which the MMA warp has consumed -- record included --
+      // since we passed empty for stage i: free to overwrite.
+      if (li + kIdxLook < my_st) prefetch(li + kIdxLook);
       ptx::cp_async_mbar_arrive_noinc(&full[stage]);  // also covers the prefetch
       ptx::cp_async_commit();
       if (threadIdx.x == 0) trace_stage<kTrace>(args, i, 0);
@@ -673,7 +699,6 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
             min(c3 - c2b, 0xffffLL);
       }
       if (threadIdx.x == 0 && (rec.w & (1 << 17))) trace_evt<kTrace>(args, rec.w & 0xffff, 1);
-      if (++stage == C::kStages) { stage = 0; phase ^= 1; }
     }
     ptx::cp_async_wait_group<0>();
   } else if (warp == kMmaWarp) {
@@ -690,11 +715,12 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     const uint32_t a_base = ptx::smem_u32(sA);
     const uint32_t b_base = ptx::smem_u32(sB);
     for (int i = 0; i < n_st; ++i) {
-      // full[stage] includes producer warp 0's cp.async arrival for stage i,
-      // which covers its prefetch of stage i's record into its ring
+      // full[stage] includes the cp.async arrival of the first warp of stage
+      // i's group, which covers its prefetch of stage i's record into its ring
       ptx::mbar_wait(&full[stage], phase);
       if (lane == 0) trace_stage<kTrace>(args, i, 1);
-      const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kIdxSlots) * kSlotInts + kRowsPerWarp);
+      const int4 rec = *reinterpret_cast<const int4 *>(sIdx + (i % kProducerGroups) * kGroupWarps * (kIdxSlots * kSlotInts) +
+                                                       ((i / kProducerGroups) % kIdxSlots) * kSlotInts + kRowsPerWarp);
       const int nq = rec.z & 0xf, nk = (rec.z >> 4) & 0xf, region = (rec.z >> 8) & 1;
       const bool w_prev = (rec.z >> 9) & 1, defer = (rec.z >> 10) & 1;
       const uint32_t n_tok = (uint32_t)nq * 64u;  // MMA N = the half's tokens
@@ -820,16 +846,22 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      if (lane == 0) ptx::bulk_wait_read<0>();  // earlier bulk stores are done reading the staging rows
       epi_sync();  // sCol visible; previous unit's staging reads done
       if (e == 0 && lane == 0) trace_evt<kTrace>(args, j - u_begin, 5);
       if (dbg<kTrace>(args, 32768)) {  // experiment: drop the accumulator unread
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
-      } else if (!kPeer && !args.accumulate && bulk_ok && !dbg<kTrace>(args, 131072)) {
+      } else if (!kPeer && !args.accumulate && bulk_ok && !dbg<kTrace>(args, 131072) &&
+                 (j + 1 < u_end || dbg<kTrace>(args, 262144))) {
+        // TMA bulk stores while the producer still gathers (the LSU is theirs);
+        // the CTA's last unit takes the LSU path below: the gathers are over,
+        // and one bulk copy per row piece costs ~30 cycles of the TMA unit
+        // (~2 us for a 128 x 256-token unit), which the 16-byte stores beat
         // TMA bulk-store epilogue (bit 131072: force the LSU path, experiment)
-        drain_unit_bulk<BN, OutT>(args, out, reinterpret_cast<uint8_t *>(sStage),
-                                  tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t, m0, nq, ucol, q, h, e,
-                                  lane);
+        drain_unit_bulk<BN, OutT, kTrace>(args, out, reinterpret_cast<uint8_t *>(sStage),
+                                          tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t, m0, nq, ucol, q,
+                                          h, e, lane, j - u_begin);
       } else if (args.accumulate || sizeof(OutT) == 4) {
         drain_unit<BN, OutT, float, 32, kPeer, kTrace>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
                                          m0, nq, ucol, q, h, e, lane, vec);

@@ -111,10 +111,10 @@ def main():
         if v.size:
             print(f"  stage {si:2d}: {np.median(v >> 48):7.0f} {np.median((v >> 32) & 0xffff):7.0f} "
                   f"{np.median((v >> 16) & 0xffff):7.0f} {np.median(v & 0xffff):7.0f}")
-    base = np.where(ep[:, :1] > 0, ep[:, :1], np.nan)
+    base = np.where(ep[:, 28:29] > 0, ep[:, 28:29], np.nan)  # bulk epilogue entry
     erel = np.where(ep > 0, ep - base, np.nan)  # SM cycles since chunk 0's TMEM load completed
-    print("epilogue chunk c of unit 0 (median over CTAs, SM cycles from chunk-0 ld): ld_done sts_done synced stored")
-    for c in range(8):
+    print("bulk epilogue of unit 0, pass c (median over CTAs, SM cycles from entry): staging free / staged / synced / issued")
+    for c in range(2):
         row = [np.nanmedian(erel[:, c * 4 + x]) if np.isfinite(erel[:, c * 4 + x]).any() else float("nan") for x in range(4)]
         print(f"  chunk {c}: " + " ".join(f"{v:8.0f}" for v in row))
     # SM clock during the launch: clock64 vs globaltimer between CTA start and end
