@@ -61,8 +61,11 @@ namespace {
 #ifndef TW_PRODUCER_GROUPS
 #define TW_PRODUCER_GROUPS 1
 #endif
+#ifndef TW_GROUP_WARPS
+#define TW_GROUP_WARPS 4
+#endif
 constexpr int kProducerGroups = TW_PRODUCER_GROUPS;
-constexpr int kGroupWarps = 4;
+constexpr int kGroupWarps = TW_GROUP_WARPS;
 constexpr int kProducerWarps = kProducerGroups * kGroupWarps;
 constexpr int kRowsPerWarp = 64 / kGroupWarps;     // kept rows of a 64-k stage per producer warp
 constexpr int kIdxLanes = kRowsPerWarp / 4;        // lanes that prefetch this warp's row indices
@@ -292,22 +295,21 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
       for (int x = 0; x < T / 32; ++x) {
         if (x > 0) load(p, x, v);
         ptx::tmem_ld_wait();
-        // fused bias / ReLU in fp32 (trainer.py:246-248), one rounding to S
-        float f[32];
+        // fused bias / ReLU in fp32 (trainer.py:246-248), in place, one
+        // rounding to S
+        if (args.bias != nullptr) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float y = __uint_as_float(v[i]);
-          if (args.bias != nullptr) {
-            y = __fadd_rn(y, bz);
+          for (int i = 0; i < 32; ++i) {
+            float y = __fadd_rn(__uint_as_float(v[i]), bz);
             if (args.relu) y = fmaxf(y, 0.f);
+            v[i] = __float_as_uint(y);
           }
-          f[i] = y;
         }
         const int c0 = (tw0 + 32 * x) * (int)sizeof(S) / 16;
 #pragma unroll
         for (int c = 0; c < 32 * (int)sizeof(S) / 16; ++c) {
           const int cc = c0 + c;
-          row[(cc & ~7) | ((cc ^ col) & 7)] = pack16<S>(f + c * (16 / (int)sizeof(S)));
+          row[(cc & ~7) | ((cc ^ col) & 7)] = pack16<S>(reinterpret_cast<const float *>(v) + c * (16 / (int)sizeof(S)));
         }
       }
     }
@@ -457,7 +459,7 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
     ptx::fence_proxy_async_smem();  // the staged rows are read by the TMA (async proxy)
     epi_sync();
     trace_epi<kTrace>(args, unit_i, p, 2, e, lane);
-    if (lane == 0) {
+    if (lane == 0 && !(kTrace && (args.debug & 2))) {  // (bit 2: experiment, no kept-row stores)
       const int tok_n = min(kPassTok, min(toks - ptok0, args.M - m0 - ptok0));
       if (tok_n > 0) {
         const uint32_t bytes = (uint32_t)tok_n * (uint32_t)sizeof(OutT);  // multiple of 16 (bulk_ok)
