@@ -79,6 +79,23 @@ int upload(T **dst, const std::vector<T> &src) {
 
 int out_size(int dtype) { return dtype == TW_F32 ? 4 : 2; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda:
+// the .so still loads on a CPU-only host)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
 // Makes the plan's GPU current for the lifetime of the guard (schedules are
 // uploaded and kernels launched on the device that holds the plan, whatever
 // device the caller has current), restoring the caller's device after.
@@ -121,6 +138,7 @@ int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, c
   if (hs.units.empty()) hs.units.assign(4, 0);
   tw_dev_schedule ds;
   ds.grid = hs.grid;
+  ds.has_contig = hs.has_contig;
   std::vector<int4> units(hs.units.size() / 4);
   for (size_t i = 0; i < units.size(); ++i)
     units[i] = make_int4(hs.units[4 * i], hs.units[4 * i + 1], hs.units[4 * i + 2], hs.units[4 * i + 3]);
@@ -364,6 +382,21 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   const uint32_t ab = hp.in_dtype == TW_BF16 ? 1u : 0u;
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 16) | ((128u >> 4) << 24);
   a.block_n = hp.block_n;
+  if (sched->has_contig) {
+    // A^T as a 2-D tensor (tokens innermost) for the TMA tile loads of
+    // consecutive-row stages: box 64 tokens x 64 rows, 128B swizzle (the
+    // layout the row gathers produce); out-of-range tokens read as zero
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)hp.a_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)lda * 2};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&a.tmap_at, hp.in_dtype == TW_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                     2, const_cast<void *>(at), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  }
   a.trace = trace;
   a.bias = bias;
   a.relu = relu;

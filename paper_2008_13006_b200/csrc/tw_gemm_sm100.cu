@@ -663,7 +663,9 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         }
       };
       const bool narrow = fast && nq * 8 < kChunks && (nq == 1 || nq == 2) && !dbg<kTrace>(args, 512);
-      if (narrow && nq == 2) {
+      if ((rec.z >> 12) & 1) {
+        // consecutive kept rows: the weight warp loads them with TMA tiles
+      } else if (narrow && nq == 2) {
         gather_rows(std::integral_constant<int, 2>{});
       } else if (narrow) {
         gather_rows(std::integral_constant<int, 4>{});
@@ -771,6 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       }
     }
   } else if (warp == kWWarp) {
+    bool ptx_dep_waited = false;
     // ------------------------------------------------ weight-block copies
     // Stage i's weight block (one 1-D TMA bulk copy of wbytes) into stage
     // slot i % kStages once the MMA has released the slot; the byte count
@@ -780,17 +783,44 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     int stage = 0;
     uint32_t phase = 0;
     for (int i0 = 0; i0 < n_st; i0 += 32) {
-      const int mine = i0 + lane < n_st ? __ldg(args.stream + (int64_t)(s_begin + i0 + lane) * kIdxInts + 64) : 0;
+      // lane l: stage i0 + l's weight offset, flags, first token and first row
+      int woff_l = 0, z_l = 0, m0_l = 0, r0_l = 0;
+      if (i0 + lane < n_st) {
+        const int32_t *rec = args.stream + (int64_t)(s_begin + i0 + lane) * kIdxInts;
+        woff_l = __ldg(rec + 64);
+        m0_l = __ldg(rec + 65);
+        z_l = __ldg(rec + 66);
+        r0_l = __ldg(rec);
+      }
       const int cnt = min(32, n_st - i0);
       for (int j = 0; j < cnt; ++j) {
-        const int woff = __shfl_sync(0xffffffffu, mine, j);
+        const int woff = __shfl_sync(0xffffffffu, woff_l, j);
+        const int z = __shfl_sync(0xffffffffu, z_l, j);
+        const int m0 = __shfl_sync(0xffffffffu, m0_l, j);
+        const int r0 = __shfl_sync(0xffffffffu, r0_l, j);
         if (lane == 0) {
           if (i0 + j >= C::kStages) ptx::mbar_wait(&empty[stage], phase ^ 1);
+          // consecutive kept rows (bit 12): the A^T rows arrive as nq TMA 2-D
+          // tiles (64 tokens x 64 rows, 128B swizzle = the gather layout)
+          // instead of row gathers; their bytes ride on the same barrier
+          const bool contig = (z >> 12) & 1;
+          const int nq = z & 0xf;
+          const uint32_t a_bytes = contig ? (uint32_t)nq * 8192u : 0u;
           if (woff < 0 || dbg<kTrace>(args, 64)) {  // reuses the previous stage's block (or experiment: no copy)
-            ptx::mbar_arrive(&full[stage]);
+            if (a_bytes) ptx::mbar_arrive_expect_tx(&full[stage], a_bytes);
+            else ptx::mbar_arrive(&full[stage]);
           } else {
-            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes);
+            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)args.wbytes + a_bytes);
             ptx::bulk_g2s(sB + stage * C::kBBytes, args.wimg + woff, (uint32_t)args.wbytes, &full[stage], keep);
+          }
+          if (contig) {
+            // A^T is produced by the previous kernel in the stream (PDL)
+            if (i0 + j == 0 || !ptx_dep_waited) {
+              asm volatile("griddepcontrol.wait;" ::: "memory");
+              ptx_dep_waited = true;
+            }
+            for (int b = 0; b < nq; ++b)
+              ptx::tma_load_2d(sA + stage * C::kABytes + b * 8192, &args.tmap_at, &full[stage], m0 + 64 * b, r0, keep);
           }
         }
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }

@@ -11,6 +11,7 @@
 
 #include "tw_b200.h"
 
+#include <cuda.h>          // CUtensorMap
 #include <vector_types.h>  // int4
 
 namespace tw {
@@ -74,6 +75,7 @@ struct HostSchedule {
   // loads never wait behind its own gathers.
   std::vector<int32_t> stream;
   std::vector<int32_t> soff;   // grid + 1
+  bool has_contig = false;     // some stage's 64 kept rows are consecutive (TMA tile loads, record bit 12)
   double makespan_ns = 0, mean_ns = 0;
 };
 int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows, int sms, int tb,
@@ -108,6 +110,8 @@ struct GemmArgs {
   int32_t n_peer;      // replicas of the output on other GPUs (tw_gemm_peers): every store goes to all
   void *peer[7];       //   of them too (NVLink peer / IPC-mapped pointers, same layout and ldc)
   int32_t no_pdl;     // 1: launch without programmatic stream serialization (TW_GEMM_NO_PDL)
+  CUtensorMap tmap_at; // A^T (a_rows x M, 16-bit) for the stages whose 64 kept rows are consecutive
+                       // (schedule has_contig): box 64 tokens x 64 rows, 128B swizzle
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };
 
@@ -124,6 +128,7 @@ uint16_t f32_to_f16_rne(float f);
 // Device copy of a schedule, cached per launch shape inside the plan.
 struct tw_dev_schedule {
   int grid = 0;
+  bool has_contig = false;
   int4 *units = nullptr;
   int32_t *off = nullptr;
   int32_t *zoff = nullptr;

@@ -228,17 +228,25 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
         const int64_t woff = t.w_off + kb * wbytes;
         if (woff > INT32_MAX) return fail(TW_ERR_UNSUPPORTED, "weight image larger than 2 GiB");
         const int32_t nk = std::min(4, t.k16 - kb * 4);
+        // a stage whose 64 kept rows are consecutive A^T rows (dense tiles:
+        // gemm_dense, 0 % sparsity) is loaded by TMA 2-D tile copies
+        // instead of row gathers: record bit 12
+        const int32_t *kx = &hp.kidx[(size_t)t.kidx_off + (size_t)kb * 64];
+        bool contig = kb * 64 + 63 < t.k_i && kx[0] >= 0 && kx[0] + 63 < hp.a_rows;
+        for (int r = 1; r < 64 && contig; ++r) contig = kx[r] == kx[0] + r;
+        s.has_contig = s.has_contig || contig;
         for (int h = 0; h < nh; ++h) {
           for (int r = 0; r < 64; ++r) {
-            const int32_t idx = hp.kidx[(size_t)t.kidx_off + (size_t)kb * 64 + (size_t)r];
+            const int32_t idx = kx[r];
             s.stream.push_back(kb * 64 + r < t.k_i && idx < hp.a_rows ? idx : -1);
           }
           // record: {weight block offset (-1: reuse the previous stage's),
           //          first token, quarters | k-steps << 4 | region << 8 |
-          //          W from the previous stage << 9 | defer the slot release << 10,
+          //          W from the previous stage << 9 | defer the slot release << 10 |
+          //          consecutive rows (TMA tile loads) << 12,
           //          half ordinal (tracing, 16 bits) | first << 16 | last << 17}
           const int32_t flags = hq[h] | (nk << 4) | (reg[h] << 8) | (h == 1 ? 1 << 9 : 0) |
-                                (pair && h == 0 ? 1 << 10 : 0);
+                                (pair && h == 0 ? 1 << 10 : 0) | (contig ? 1 << 12 : 0);
           s.stream.insert(s.stream.end(),
                           {h == 0 ? (int32_t)woff : -1, hm0[h], flags,
                            ((half_no + h) & 0xffff) | (kb == 0 ? 1 << 16 : 0) | (kb == t.nkb - 1 ? 1 << 17 : 0)});

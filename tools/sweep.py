@@ -57,7 +57,7 @@ def rows(quick: bool):
          ("C2a-het", 4096, 768, 3072, 0.75, None), ("C5-het@0.75", 16384, 1024, 4096, 0.75, None)]
     for s in (0.5, 0.75, 0.9):
         r.append((f"NMT@{s:g}", 4096, 1024, 2048, s, None))
-    for s in ([0.0, 0.5, 0.75, 0.9] if quick else [0.0, 0.1, 0.25, 0.5, 0.75, 0.9]):
+    for s in ([0.0, 0.25, 0.4, 0.5, 0.75, 0.9] if quick else [0.0, 0.1, 0.25, 0.4, 0.5, 0.75, 0.9]):
         r.append((f"C5@{s:g}", 16384, 1024, 4096, s, None))
     vgg = VGG[1::3] if quick else VGG
     for s in (0.5, 0.75):
