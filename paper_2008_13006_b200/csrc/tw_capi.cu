@@ -139,6 +139,7 @@ int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, c
   tw_dev_schedule ds;
   ds.grid = hs.grid;
   ds.has_contig = hs.has_contig;
+  ds.has_tma_rows = hs.has_tma_rows;
   std::vector<int4> units(hs.units.size() / 4);
   for (size_t i = 0; i < units.size(); ++i)
     units[i] = make_int4(hs.units[4 * i], hs.units[4 * i + 1], hs.units[4 * i + 2], hs.units[4 * i + 3]);
@@ -396,6 +397,26 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
                      2, const_cast<void *>(at), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  }
+  const int ob = out_size(out_dtype);
+  if (sched->has_tma_rows && !accum && n_peer == 0 && (reinterpret_cast<uintptr_t>(ct) & 15) == 0 &&
+      (ldc * ob) % 16 == 0) {
+    // C^T as a 2-D tensor (tokens innermost) for the epilogue's TMA tensor
+    // stores: box 128 B of tokens x 128 rows, 128B swizzle (the staging
+    // layout); tokens >= M are clipped by the TMA unit
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ldc * ob)};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / ob), 128};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapDataType dt = out_dtype == TW_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : out_dtype == TW_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUresult r = enc(&a.tmap_out, dt, 2, ct, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed: " + std::to_string((int)r));
+    a.tma_out = 1;
   }
   a.trace = trace;
   a.bias = bias;

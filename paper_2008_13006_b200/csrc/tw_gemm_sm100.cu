@@ -476,6 +476,70 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
   }
 }
 
+// Epilogue of one unit whose tile owns 128 CONSECUTIVE C^T rows (unit flag
+// bit 1, G = 128): the staged unit leaves as 2-D TMA tensor stores -- one
+// instruction per 128-byte-wide box of 128 rows (4 per 256-token pass of
+// 16-bit output, 4 per 128-token pass of fp32) instead of one bulk copy per
+// row piece (128 per pass, ~30 TMA cycles each).  The staging is the box
+// layout with the 128B swizzle: box b at sStg + b * 16 KB, row r at + r * 128,
+// 16-byte chunk c at ((c ^ r) & 7) * 16 -- the 32 rows of a tcgen05.ld (one
+// per lane) hit 8 distinct bank groups, so the 16-byte shared stores are
+// conflict-free.  Warp (q, h): rows 32q.., tokens h * pass/2 ..; lane 0 of
+// warps 0..3 issues box e of the pass.  Tokens >= M are clipped by the TMA.
+template <typename OutT, bool kTrace>
+__device__ __forceinline__ void drain_unit_tma(const GemmArgs &args, uint8_t *sStg, uint32_t t_acc, uint64_t *tempty,
+                                               const TileMeta &t, int m0, int nq, int row0, int q, int h, int e,
+                                               int lane) {
+  constexpr int kBoxTok = 128 / (int)sizeof(OutT);      // tokens per box row (128 B)
+  constexpr int kPassTok = 4 * kBoxTok;                  // 4 boxes (64 KB) per pass
+  constexpr int kChunks = 32 * (int)sizeof(OutT) / 16;  // 16-byte chunks per 32 tokens
+  const int toks = nq * 64;
+  const int n_pass = (toks + kPassTok - 1) / kPassTok;
+  const int row = q * 32 + lane;  // staged row = tile column of this thread
+  const uint32_t t_base = t_acc + ((uint32_t)(q * 32) << 16);
+  float bz = 0.f;
+  if (args.bias != nullptr) bz = __ldg(args.bias + row0 + row);
+  for (int p = 0; p < n_pass; ++p) {
+    if (lane == 0) ptx::bulk_wait_read<0>();  // earlier stores are done reading the staging boxes
+    epi_sync();
+    const int ptok0 = p * kPassTok;
+    const int pt = min(kPassTok, toks - ptok0);  // multiple of 64 tokens
+    const int tw0 = h * (pt / 2), tw1 = tw0 + pt / 2;
+#pragma unroll
+    for (int x = 0; x < kPassTok / 2 / 32; ++x) {
+      const int tl = tw0 + 32 * x;  // token within the pass
+      if (tl >= tw1) break;         // warp-uniform
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)(ptok0 + tl), v);
+      ptx::tmem_ld_wait();
+      if (args.bias != nullptr) {  // trainer.py:246-248, in fp32 before the one rounding
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float z = __fadd_rn(__uint_as_float(v[i]), bz);
+          if (args.relu) z = fmaxf(z, 0.f);
+          v[i] = __float_as_uint(z);
+        }
+      }
+      uint8_t *box = sStg + (tl / kBoxTok) * 16384 + row * 128;
+      const int c0 = (tl % kBoxTok) * (int)sizeof(OutT) / 16;
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c)
+        reinterpret_cast<uint4 *>(box)[((c0 + c) ^ row) & 7] =
+            pack16<OutT>(reinterpret_cast<const float *>(v) + c * (16 / (int)sizeof(OutT)));
+    }
+    if (p == n_pass - 1) {  // every TMEM read of the unit is done: hand the accumulator back
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(tempty);
+    }
+    ptx::fence_proxy_async_smem();  // the staging boxes are read by the TMA (async proxy)
+    epi_sync();
+    if (lane == 0 && e < 4 && e * kBoxTok < pt && !(kTrace && (args.debug & 2))) {
+      ptx::tma_store_2d(&args.tmap_out, sStg + e * 16384, m0 + ptok0 + e * kBoxTok, row0);
+      ptx::bulk_commit();
+    }
+  }
+}
+
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
 // committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
@@ -884,6 +948,11 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (dbg<kTrace>(args, 32768)) {  // experiment: drop the accumulator unread
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
+      } else if (BN <= 128 && !kPeer && args.tma_out && (su.w & 2) && !dbg<kTrace>(args, 524288)) {
+        // 128 consecutive output rows: 2-D TMA tensor stores (every unit,
+        // the CTA's last included: 4 store instructions per pass)
+        drain_unit_tma<OutT, kTrace>(args, reinterpret_cast<uint8_t *>(sStage), tmem_base + (uint32_t)(acc * C::kAccCols),
+                                     &tempty[acc], t, m0, nq, ucol[0], q, h, e, lane);
       } else if (!kPeer && !args.accumulate && bulk_ok && !dbg<kTrace>(args, 131072) &&
                  (j + 1 < u_end || dbg<kTrace>(args, 262144))) {
         // TMA bulk stores while the producer still gathers (the LSU is theirs);

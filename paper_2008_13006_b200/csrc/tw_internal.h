@@ -76,6 +76,7 @@ struct HostSchedule {
   std::vector<int32_t> stream;
   std::vector<int32_t> soff;   // grid + 1
   bool has_contig = false;     // some stage's 64 kept rows are consecutive (TMA tile loads, record bit 12)
+  bool has_tma_rows = false;   // some unit's tile has 128 consecutive output rows (unit flag bit 1)
   double makespan_ns = 0, mean_ns = 0;
 };
 int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows, int sms, int tb,
@@ -112,6 +113,10 @@ struct GemmArgs {
   int32_t no_pdl;     // 1: launch without programmatic stream serialization (TW_GEMM_NO_PDL)
   CUtensorMap tmap_at; // A^T (a_rows x M, 16-bit) for the stages whose 64 kept rows are consecutive
                        // (schedule has_contig): box 64 tokens x 64 rows, 128B swizzle
+  CUtensorMap tmap_out; // C^T (M x output rows) for the epilogue's 2-D TMA tensor stores of tiles
+                        // whose 128 output rows are consecutive (unit flag bit 1): box 128 B x 128 rows,
+                        // 128B swizzle; valid when tma_out != 0
+  int32_t tma_out;
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };
 
@@ -129,6 +134,7 @@ uint16_t f32_to_f16_rne(float f);
 struct tw_dev_schedule {
   int grid = 0;
   bool has_contig = false;
+  bool has_tma_rows = false;
   int4 *units = nullptr;
   int32_t *off = nullptr;
   int32_t *zoff = nullptr;

@@ -222,8 +222,16 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
       int hq[2] = {pair ? qh : u.nq, pair ? u.nq - qh : 0};
       int hm0[2] = {u.m0, u.m0 + qh * 64};
       int reg[2] = {half_no & 1, (half_no + 1) & 1};
-      // epilogue units: one per half, in completion order
-      for (int h = 0; h < nh; ++h) s.units.insert(s.units.end(), {u.tile, hm0[h], hq[h], reg[h]});
+      // epilogue units: one per half, in completion order; flag bit 1: the
+      // tile's 128 output rows are consecutive C^T rows, so the epilogue
+      // stores the unit with 2-D TMA tensor stores (4 boxes per 256 tokens)
+      // instead of one bulk copy per row piece
+      bool rows_consecutive = t.n_i == 128 && hp.block_n == 128;
+      for (int r = 1; r < t.n_i && rows_consecutive; ++r)
+        rows_consecutive = hp.colids[(size_t)t.col_off + r] == hp.colids[(size_t)t.col_off] + r;
+      for (int h = 0; h < nh; ++h)
+        s.units.insert(s.units.end(), {u.tile, hm0[h], hq[h], reg[h] | (rows_consecutive ? 2 : 0)});
+      s.has_tma_rows = s.has_tma_rows || rows_consecutive;
       for (int kb = 0; kb < t.nkb; ++kb) {
         const int64_t woff = t.w_off + kb * wbytes;
         if (woff > INT32_MAX) return fail(TW_ERR_UNSUPPORTED, "weight image larger than 2 GiB");
