@@ -122,6 +122,14 @@ typedef struct tw_plan_info {
  *   gemm_tw bit for bit on ANY fp32 weights, not only bf16-representable ones. */
 #define TW_PLAN_SPLIT3 1
 #define TW_PLAN_F32_WEIGHTS 2
+/* TW_PLAN_DENSE_PAD: every live tile keeps ALL K rows, the pruned ones with
+ *   zero weights (the same products: a pruned weight contributes 0 * a).
+ *   Such a plan runs on the 2-SM kernel (tcgen05 cta_group::2, 256 output
+ *   columns x 256 tokens per CTA pair, A^T by TMA tiles): the choice for
+ *   near-dense patterns, where gathering the kept rows costs more than the
+ *   MMAs on the pruned ones.  Non-finite activations in a
+ *   tile's pruned rows give NaN there (0 * Inf), as in any dense GEMM. */
+#define TW_PLAN_DENSE_PAD 4
 
 /* Build a plan from the reference's compact form (the same arrays as
  * tw_compact's outputs plus the pattern) and upload it to the current

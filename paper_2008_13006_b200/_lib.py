@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtw_b200.
 TW_OK, TW_ERR_DIMENSION, TW_ERR_FORMAT = 0, 1, 2
 TW_F32, TW_BF16, TW_F16 = 0, 1, 2
 TW_ROW_MAJOR, TW_COL_MAJOR = 0, 1
-TW_PLAN_SPLIT3, TW_PLAN_F32_WEIGHTS = 1, 2
+TW_PLAN_SPLIT3, TW_PLAN_F32_WEIGHTS, TW_PLAN_DENSE_PAD = 1, 2, 4
 
 # every symbol include/tw_b200.h declares: name -> (restype, argtypes)
 _p = ctypes.c_void_p

@@ -12,6 +12,8 @@
 namespace tw {
 int tokens_per_unit(int block_n);
 cudaError_t launch_tw_gemm_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream);
+cudaError_t launch_tw_pair_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream);
+int pair_clusters_max(int out_dtype);
 cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
                         cudaStream_t s);
 cudaError_t launch_spmm(const void *at, int at_dtype, int64_t m, int64_t k, int64_t lda, int64_t col_begin, int64_t n_cols,
@@ -122,24 +124,42 @@ void free_schedule(tw_dev_schedule &ds) {
   ds = tw_dev_schedule{};
 }
 
+// CTA pairs of K4 that fit the device at once (persistent grid), per output
+// dtype; 0 when the kernel cannot be launched as a cluster here.
+int pair_cluster_count(int out_dtype) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;  // (device, dtype)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, out_dtype});
+  if (it != cache.end()) return it->second;
+  const int n = pair_clusters_max(out_dtype);
+  cache[{dev, out_dtype}] = n;
+  return n;
+}
+
 // Static schedule for (M, output width, zero rows on/off), built once per
 // launch shape and cached on the plan (uploaded to the plan's device).
-int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, const tw_dev_schedule **out) {
+int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, const tw_dev_schedule **out,
+                 int pair_clusters = 0) {
   std::lock_guard<std::mutex> lk(p->sched_mu);
-  const auto key = std::make_tuple(m, ob, zero_rows ? 1 : 0);
+  const auto key = std::make_tuple(m, ob + (pair_clusters > 0 ? 100 : 0), zero_rows ? 1 : 0);
   auto it = p->sched.find(key);
   if (it != p->sched.end()) {
     *out = &it->second;
     return TW_OK;
   }
   HostSchedule hs;
-  int rc = build_schedule(p->host, m, ob, zero_rows, sms, tokens_per_unit(p->host.block_n), hs);
+  int rc = pair_clusters > 0 ? build_pair_schedule(p->host, m, zero_rows, pair_clusters, hs)
+                             : build_schedule(p->host, m, ob, zero_rows, sms, tokens_per_unit(p->host.block_n), hs);
   if (rc) return rc;
   if (hs.units.empty()) hs.units.assign(4, 0);
   tw_dev_schedule ds;
   ds.grid = hs.grid;
   ds.has_contig = hs.has_contig;
   ds.has_tma_rows = hs.has_tma_rows;
+  ds.pair = hs.pair;
   std::vector<int4> units(hs.units.size() / 4);
   for (size_t i = 0; i < units.size(); ++i)
     units[i] = make_int4(hs.units[4 * i], hs.units[4 * i + 1], hs.units[4 * i + 2], hs.units[4 * i + 3]);
@@ -191,6 +211,7 @@ int tw_plan_create_ex(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const in
                            col_end, p->host, flags);
   if (rc) { delete p; return rc; }
   cudaGetDevice(&p->device);
+  p->pair_ok = pair_eligible(p->host);
   if ((rc = upload(&p->d_tiles, p->host.tiles)) || (rc = upload(&p->d_kidx, p->host.kidx)) ||
       (rc = upload(&p->d_colids, p->host.colids)) || (rc = upload(&p->d_zero, p->host.zero_rows)) ||
       (rc = upload(&p->d_wimg, p->host.wimg)) || (rc = upload(&p->d_w32, p->host.w32)) ||
@@ -356,7 +377,18 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   const tw_dev_schedule *sched = nullptr;
   const bool accum = (accumulate & TW_GEMM_ACCUMULATE) != 0;
   const bool keep_pruned = (accumulate & TW_GEMM_KEEP_PRUNED) != 0;
-  if ((rc = get_schedule(p, m, out_size(out_dtype), !accum && !keep_pruned, sms, &sched))) return rc;
+  const int ob = out_size(out_dtype);
+  // K4 (CTA-pair kernel) for plans whose tiles keep every row in order, when
+  // the output takes 16-byte bulk / TMA stores (TW_B200_PAIR=0 disables)
+  static const bool pair_env = [] {
+    const char *e = std::getenv("TW_B200_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  int pair_clusters = 0;
+  if (pair_env && p->pair_ok && !accum && n_peer == 0 && trace == nullptr && hp.a_rows == hp.k &&
+      (reinterpret_cast<uintptr_t>(ct) & 15) == 0 && (ldc * ob) % 16 == 0 && (m * ob) % 16 == 0)
+    pair_clusters = pair_cluster_count(out_dtype);
+  if ((rc = get_schedule(p, m, ob, !accum && !keep_pruned, sms, &sched, pair_clusters))) return rc;
   GemmArgs a{};
   a.tiles = p->d_tiles;
   a.kidx = p->d_kidx;
@@ -383,7 +415,7 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   const uint32_t ab = hp.in_dtype == TW_BF16 ? 1u : 0u;
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | (1u << 16) | ((128u >> 4) << 24);
   a.block_n = hp.block_n;
-  if (sched->has_contig) {
+  if (sched->has_contig || sched->pair) {
     // A^T as a 2-D tensor (tokens innermost) for the TMA tile loads of
     // consecutive-row stages: box 64 tokens x 64 rows, 128B swizzle (the
     // layout the row gathers produce); out-of-range tokens read as zero
@@ -398,7 +430,20 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   }
-  const int ob = out_size(out_dtype);
+  if (sched->pair) {
+    // the weight image as a 2-D tensor of 128-byte rows (already swizzled:
+    // copied verbatim), box = one 128-row weight block
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {64, (cuuint64_t)(hp.wimg.size() / 128)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&a.tmap_w, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->d_wimg, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled (weights) failed: " + std::to_string((int)r));
+  }
   if (sched->has_tma_rows && !accum && n_peer == 0 && (reinterpret_cast<uintptr_t>(ct) & 15) == 0 &&
       (ldc * ob) % 16 == 0) {
     // C^T as a 2-D tensor (tokens innermost) for the epilogue's TMA tensor
@@ -433,7 +478,8 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
     a.debug = dbg ? std::atoi(dbg) : 0;
   }
   const int grid = sched->grid;
-  cudaError_t e = launch_tw_gemm_sm100(a, out_dtype, grid, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = sched->pair ? launch_tw_pair_sm100(a, out_dtype, grid, reinterpret_cast<cudaStream_t>(stream))
+                              : launch_tw_gemm_sm100(a, out_dtype, grid, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tw_gemm launch");
   return TW_OK;
 }

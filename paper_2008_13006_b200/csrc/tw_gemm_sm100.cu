@@ -451,7 +451,7 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
           dst[c] = pack16<OutT>(reinterpret_cast<const float *>(v) + c * (16 / (int)sizeof(OutT)));
       }
     }
-    if (p == n_pass - 1) {  // every TMEM read of the unit is done: hand the accumulator back
+    if (p == n_pass - 1 && tempty != nullptr) {  // every TMEM read of the unit is done: hand the accumulator back
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty);
     }
@@ -527,7 +527,7 @@ __device__ __forceinline__ void drain_unit_tma(const GemmArgs &args, uint8_t *sS
         reinterpret_cast<uint4 *>(box)[((c0 + c) ^ row) & 7] =
             pack16<OutT>(reinterpret_cast<const float *>(v) + c * (16 / (int)sizeof(OutT)));
     }
-    if (p == n_pass - 1) {  // every TMEM read of the unit is done: hand the accumulator back
+    if (p == n_pass - 1 && tempty != nullptr) {  // every TMEM read of the unit is done: hand the accumulator back
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty);
     }
@@ -994,6 +994,241 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
   }
 }
 
+// ====================================================================== K4
+// CTA-pair kernel for plans whose tiles keep every K row in order (dense
+// patterns, TW_PLAN_DENSE_PAD plans of near-dense patterns).  A cluster of 2
+// CTAs on one TPC computes 256 output columns (the two tiles of a pair) x
+// 256 tokens per unit with tcgen05.mma.cta_group::2 (M = 256, N = 256): CTA
+// r holds the 128 x 64 weight block of its tile (A operand rows 128r..) and
+// tokens 128r..128r+127 of the A^T stage (B operand columns), so each SM
+// loads 32 KB per 64-k stage for 2 x 128 x 256 x 64 MACs -- 2/3 of the bytes
+// per MMA of K2's 128-column unit, where the A^T stage is read once per tile.
+// All operands come by TMA tile loads (no row gathers: every row is kept).
+// Warps: 0 TMA loads (both CTAs; completion counted on the LEADER's full
+// barrier), 1 MMA (leader only; commits multicast to both CTAs), 2..9
+// epilogue (each CTA drains its own TMEM: its tile's 128 rows x 256 tokens,
+// K2's drain functions), zero rows as in K2.
+constexpr int kPairStages = 4;
+constexpr int kPairThreads = 10 * 32;
+constexpr uint32_t kPairStageBytes = 32768;  // 16 KB weight block + 16 KB A^T half
+constexpr uint32_t kPairStagingBytes = 69632;
+constexpr uint32_t kPairSmem = 1024 + kPairStages * kPairStageBytes + kPairStagingBytes + 2 * 128 * 4 + 256 + 8192;
+static_assert(kPairSmem <= 232448u, "K4 shared memory budget");
+
+template <typename OutT>
+__global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __grid_constant__ GemmArgs args) {
+  constexpr int S = kPairStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t *sW = smem;                        // S x 16 KB weight blocks (K-major SW128, host-swizzled)
+  uint8_t *sA = smem + S * 16384;            // S x 16 KB A^T halves (2 blocks of 64 tokens, SW128)
+  uint8_t *sStage = sA + S * 16384;          // epilogue staging (1 KB aligned)
+  int32_t *sCol = reinterpret_cast<int32_t *>(sStage + kPairStagingBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sCol + 2 * 128);
+  uint64_t *empty = full + S;
+  uint64_t *tfull = empty + S;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint8_t *sZero = reinterpret_cast<uint8_t *>(full) + 256;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_rank();
+  const int cl = blockIdx.x >> 1;
+  const int u_begin = __ldg(args.sched_off + cl);
+  const int u_end = __ldg(args.sched_off + cl + 1);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&full[s], 1);   // the leader's expect_tx arrival (+ both CTAs' bytes)
+      ptx::mbar_init(&empty[s], 1);  // the pair MMA's multicast commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 16);  // 8 epilogue warps x 2 CTAs
+    }
+    ptx::fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < 8192 / 16; i += kPairThreads) reinterpret_cast<uint4 *>(sZero)[i] = make_uint4(0, 0, 0, 0);
+  ptx::fence_proxy_async_smem();
+  if (warp == 1) ptx::tmem_alloc2<512>(tmem_holder);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // both CTAs' barriers exist before any cross-CTA signal
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA loads (both CTAs)
+    if (ptx::elect_one()) {
+      const uint32_t full_lead = ptx::mapa(ptx::smem_u32(full), 0);
+      const uint64_t keep = ptx::policy_evict_last();
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // A^T may come from the previous kernel
+      int stage = 0, n = 0;
+      uint32_t phase = 0;
+      for (int j = u_begin; j < u_end; ++j) {
+        const int4 su = __ldg(args.sched + j);
+        const int tile = (rank == 1 && su.y >= 0) ? su.y : su.x;  // no tile of its own: a copy of the leader's
+        const TileMeta t = args.tiles[tile];
+        const int tok = su.z + (int)rank * 128;
+        for (int kb = 0; kb < t.nkb; ++kb, ++n) {
+          if (n >= S) ptx::mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 4u * 16384u);
+          const uint32_t bar = full_lead + (uint32_t)stage * 8u;
+          ptx::tma_load_2d_pair(sW + stage * 16384, &args.tmap_w, bar, 0,
+                                (int32_t)((t.w_off + (int64_t)kb * 16384) >> 7), keep);
+          ptx::tma_load_2d_pair(sA + stage * 16384, &args.tmap_at, bar, tok, kb * 64, keep);
+          ptx::tma_load_2d_pair(sA + stage * 16384 + 8192, &args.tmap_at, bar, tok + 64, kb * 64, keep);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+      // drain: the pair MMA's last commits arrive on this CTA's empty
+      // barriers -- they must land before the CTA (and its shared memory) exits
+      for (int x = 0; x < S && x < n; ++x) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ pair MMA (leader)
+    if (rank == 0) {
+      // M = 256 ([24,29) = 16), N = 256 ([17,23) = 32)
+      const uint32_t idesc = (args.idesc & ~(0x1Fu << 24)) | (16u << 24) | (32u << 17);
+      const uint32_t w_base = ptx::smem_u32(sW), a_base = ptx::smem_u32(sA);
+      int stage = 0;
+      uint32_t phase = 0, use[2] = {0, 0};
+      for (int j = u_begin; j < u_end; ++j) {
+        const int acc = (j - u_begin) & 1;
+        const TileMeta t = args.tiles[__ldg(args.sched + j).x];
+        ptx::mbar_wait_cluster(&tempty[acc], (use[acc] & 1) ^ 1);  // both CTAs drained this accumulator
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
+        for (int kb = 0; kb < t.nkb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t adesc = ptx::make_sw128_desc(w_base + stage * 16384 + kk * 32, 16, 1024);
+              const uint64_t bdesc = ptx::make_sw128_desc(a_base + stage * 16384 + kk * 2048, 8192, 1024);
+              ptx::mma2_f16_ss(d_tmem, adesc, bdesc, idesc, (kb | kk) ? 1u : 0u);
+            }
+            ptx::mma2_commit_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        if (ptx::elect_one()) ptx::mma2_commit_mc(&tfull[acc], 0x3);
+        __syncwarp();
+        ++use[acc];
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (8 warps)
+    const int e = warp - 2;  // 0..7
+    const int et = e * 32 + lane;
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const int h = e >> 2;
+    const uint32_t tempty_lead = ptx::mapa(ptx::smem_u32(tempty), 0);
+    int zr = __ldg(args.zero_off + blockIdx.x);
+    const int z1 = args.keep_pruned ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
+    volatile int32_t *s_zdone = reinterpret_cast<volatile int32_t *>(tmem_holder + 1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the output may be read / written by the previous kernel
+    uint32_t use[2] = {0, 0};
+    OutT *out = reinterpret_cast<OutT *>(args.out);
+    for (int j = u_begin; j < u_end; ++j) {
+      const int4 su = __ldg(args.sched + j);
+      const int acc = (j - u_begin) & 1;
+      const int tile = rank == 1 ? su.y : su.x;
+      const TileMeta t = args.tiles[tile < 0 ? su.x : tile];
+      int32_t *ucol = sCol + ((j - u_begin) & 1) * 128;
+      if (et < 128) ucol[et] = (tile >= 0 && et < t.n_i) ? __ldg(args.colids + t.col_off + et) : -1;
+      while (e == 0 && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], use[acc] & 1)) {
+        if (lane == 0) ptx::bulk_wait_read<0>();
+        zero_row_bulk<OutT, false>(args, __ldg(args.zero_rows + zr), lane, true, true, sZero, 8192);
+        ++zr;
+      }
+      ptx::mbar_wait(&tfull[acc], use[acc] & 1);
+      ptx::tc_fence_after();
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      epi_sync();
+      const uint32_t t_acc = tmem_base + (uint32_t)(acc * 256);
+      if (tile >= 0) {
+        if (args.tma_out && ((su.w >> rank) & 1))
+          drain_unit_tma<OutT, false>(args, sStage, t_acc, nullptr, t, su.z, 4, ucol[0], q, h, e, lane);
+        else
+          drain_unit_bulk<128, OutT, false>(args, out, sStage, t_acc, nullptr, t, su.z, 4, ucol, q, h, e, lane, 0);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(tempty_lead + (uint32_t)acc * 8u);
+      ++use[acc];
+    }
+    if (e == 0 && lane == 0) *s_zdone = zr;
+    epi_sync();
+    for (zr = *s_zdone + e; zr < z1; zr += 8)
+      zero_row_bulk<OutT, false>(args, __ldg(args.zero_rows + zr), lane, true, true, sZero, 8192);
+    if (lane == 0) ptx::bulk_wait_read<0>();
+  }
+
+  __syncthreads();
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // the peer is done with this CTA's shared memory and barriers
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2<512>(tmem_base);
+  }
+}
+
+template <typename OutT>
+cudaError_t launch_pair(const GemmArgs &args, int grid, cudaStream_t stream) {
+  auto kern = tw_pair_sm100_kernel<OutT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem);
+  if (e != cudaSuccess) return e;
+  static const bool pdl = [] {
+    const char *v = std::getenv("TW_B200_PDL");
+    return !(v && v[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kPairThreads);
+  cfg.dynamicSmemBytes = kPairSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && !args.no_pdl) ? 2 : 1;
+  e = cudaLaunchKernelEx(&cfg, kern, args);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+template <typename OutT>
+int pair_clusters_of() {
+  auto kern = tw_pair_sm100_kernel<OutT>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(kPairThreads);
+  cfg.dynamicSmemBytes = kPairSmem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return 0;
+  return n;
+}
+
 template <int BN, typename OutT, bool kPeer, bool kTrace>
 cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
   auto kern = tw_gemm_sm100_kernel<BN, OutT, kPeer, kTrace>;
@@ -1040,6 +1275,24 @@ cudaError_t launch_out(const GemmArgs &args, int grid, cudaStream_t stream) {
 }  // namespace
 
 int tokens_per_unit(int block_n) { return block_n <= 128 ? Cfg<128>::TB : Cfg<256>::TB; }
+
+cudaError_t launch_tw_pair_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream) {
+  switch (out_dtype) {
+    case TW_F32: return launch_pair<float>(args, grid, stream);
+    case TW_BF16: return launch_pair<__nv_bfloat16>(args, grid, stream);
+    case TW_F16: return launch_pair<__half>(args, grid, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int pair_clusters_max(int out_dtype) {
+  switch (out_dtype) {
+    case TW_F32: return pair_clusters_of<float>();
+    case TW_BF16: return pair_clusters_of<__nv_bfloat16>();
+    case TW_F16: return pair_clusters_of<__half>();
+  }
+  return 0;
+}
 
 cudaError_t launch_tw_gemm_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream) {
   switch (out_dtype) {

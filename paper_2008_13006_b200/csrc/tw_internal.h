@@ -77,10 +77,19 @@ struct HostSchedule {
   std::vector<int32_t> soff;   // grid + 1
   bool has_contig = false;     // some stage's 64 kept rows are consecutive (TMA tile loads, record bit 12)
   bool has_tma_rows = false;   // some unit's tile has 128 consecutive output rows (unit flag bit 1)
+  bool pair = false;           // K4 (CTA-pair) schedule: off is per cluster, no stage stream
   double makespan_ns = 0, mean_ns = 0;
 };
 int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows, int sms, int tb,
                    HostSchedule &s);
+// K4 (CTA-pair kernel): every live tile keeps all K rows in order (a dense
+// pattern or TW_PLAN_DENSE_PAD) with 128-row weight blocks.
+bool pair_eligible(const HostPlan &hp);
+// K4 schedule: units {tile of CTA rank 0, tile of rank 1 (-1: none), first
+// token, consecutive-rows flags (bit r: rank r's tile owns 128 consecutive
+// C^T rows)} of 256 tokens, dealt round-robin to `clusters` CTA pairs
+// (off: clusters + 1); zero rows split evenly over the 2 * clusters CTAs.
+int build_pair_schedule(const HostPlan &hp, int64_t m, bool zero_rows, int clusters, HostSchedule &s);
 
 // Kernel arguments of the persistent TW-GEMM (tw_gemm_sm100.cu).
 struct GemmArgs {
@@ -117,6 +126,7 @@ struct GemmArgs {
                         // whose 128 output rows are consecutive (unit flag bit 1): box 128 B x 128 rows,
                         // 128B swizzle; valid when tma_out != 0
   int32_t tma_out;
+  CUtensorMap tmap_w;  // K4: the weight image as 2-D (128-byte rows), box 128 B x 128 rows, no swizzle
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };
 
@@ -135,6 +145,7 @@ struct tw_dev_schedule {
   int grid = 0;
   bool has_contig = false;
   bool has_tma_rows = false;
+  bool pair = false;  // K4 schedule (grid = 2 x clusters)
   int4 *units = nullptr;
   int32_t *off = nullptr;
   int32_t *zoff = nullptr;
@@ -153,6 +164,7 @@ struct tw_plan {
   uint8_t *d_wimg = nullptr;
   float *d_w32 = nullptr;        // TW_PLAN_F32_WEIGHTS
   int64_t *d_w32_off = nullptr;
+  bool pair_ok = false;          // K4-eligible (pair_eligible)
   mutable std::mutex sched_mu;
   mutable std::map<std::tuple<int64_t, int, int>, tw_dev_schedule> sched;  // (M, out bytes, zero rows on)
 };

@@ -63,8 +63,11 @@ int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int6
                     const int64_t *sub_off, int in_dtype, int64_t col_begin, int64_t col_end,
                     HostPlan &hp, int flags) {
   if (k < 1 || n < 1 || g < 1) return fail(TW_ERR_DIMENSION, "bad pattern dims");
-  if (flags & ~(TW_PLAN_SPLIT3 | TW_PLAN_F32_WEIGHTS)) return fail(TW_ERR_ARG, "unknown plan flags");
+  if (flags & ~(TW_PLAN_SPLIT3 | TW_PLAN_F32_WEIGHTS | TW_PLAN_DENSE_PAD)) return fail(TW_ERR_ARG, "unknown plan flags");
   const bool split = (flags & TW_PLAN_SPLIT3) != 0;
+  const bool pad = (flags & TW_PLAN_DENSE_PAD) != 0;
+  if (pad && (flags & (TW_PLAN_SPLIT3 | TW_PLAN_F32_WEIGHTS)))
+    return fail(TW_ERR_ARG, "TW_PLAN_DENSE_PAD does not combine with TW_PLAN_SPLIT3 / TW_PLAN_F32_WEIGHTS");
   if (split && in_dtype != TW_BF16) return fail(TW_ERR_ARG, "TW_PLAN_SPLIT3 needs TW_BF16 operands");
   if (g > 256) return fail(TW_ERR_UNSUPPORTED, "tile width G > 256 is not supported by the sm_100a kernel");
   if (in_dtype != TW_BF16 && in_dtype != TW_F16) return fail(TW_ERR_ARG, "in_dtype must be TW_BF16 or TW_F16");
@@ -131,10 +134,15 @@ int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int6
   // of A^T (= Ah) with Wh, rows r + K (= Al, the second half of the 2K-row
   // split operand tw_prep_activations_split writes) with Wh, rows r with Wl.
   const int reps = split ? 3 : 1;
+  std::vector<int32_t> kpos;  // TW_PLAN_DENSE_PAD: row -> position in the tile's kept list, or -1
   for (const Live &L : live) {
     TileMeta m{};
     const int64_t n_i = L.j1 - L.j0;
-    const int64_t kx = L.k_i * reps;  // kept rows as the kernel sees them
+    const int64_t kx = pad ? k : L.k_i * reps;  // kept rows as the kernel sees them
+    if (pad) {
+      kpos.assign((size_t)k, -1);
+      for (size_t r = 0; r < L.rows.size(); ++r) kpos[(size_t)L.rows[r]] = (int32_t)r;
+    }
     m.n_i = (int32_t)n_i;
     m.k_i = (int32_t)kx;
     m.k16 = (int32_t)((kx + 15) / 16);
@@ -144,7 +152,7 @@ int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int6
     m.w_off = (int64_t)hp.wimg.size();
     for (int64_t r = 0; r < (int64_t)m.nkb * 64; ++r) {
       int32_t idx = (int32_t)hp.a_rows;  // pad: out-of-range row -> zeros
-      if (r < kx) idx = L.rows[(size_t)(r % L.k_i)] + (r / L.k_i == 1 ? (int32_t)k : 0);
+      if (r < kx) idx = pad ? (int32_t)r : L.rows[(size_t)(r % L.k_i)] + (r / L.k_i == 1 ? (int32_t)k : 0);
       hp.kidx.push_back(idx);
     }
     const int64_t c0 = col_off[L.src];
@@ -167,8 +175,8 @@ int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int6
           uint16_t *dst = (uint16_t *)(blk + j * 128 + ((c ^ (j & 7)) * 16));
           for (int e = 0; e < 8; ++e) {
             const int64_t kk = (int64_t)kb * 64 + c * 8 + e;
-            if (kk >= kx) { dst[e] = 0; continue; }
-            const float v = colv[kk % ktile];
+            if (kk >= kx || (pad && kpos[(size_t)kk] < 0)) { dst[e] = 0; continue; }
+            const float v = colv[pad ? kpos[(size_t)kk] : kk % ktile];
             if (!split) {
               dst[e] = in_dtype == TW_BF16 ? f32_to_bf16_rne(v) : f32_to_f16_rne(v);
             } else {

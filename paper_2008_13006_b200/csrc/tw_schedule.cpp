@@ -274,4 +274,60 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
   return TW_OK;
 }
 
+bool pair_eligible(const HostPlan &hp) {
+  if (hp.tiles.empty() || (hp.flags & TW_PLAN_SPLIT3) || hp.block_n != 128 || hp.wrows != 128) return false;
+  for (const TileMeta &t : hp.tiles) {
+    if (t.k_i != hp.k) return false;
+    const int32_t *kx = &hp.kidx[(size_t)t.kidx_off];
+    for (int64_t r = 0; r < hp.k; ++r)
+      if (kx[r] != (int32_t)r) return false;
+  }
+  return true;
+}
+
+int build_pair_schedule(const HostPlan &hp, int64_t m, bool zero_rows, int clusters, HostSchedule &s) {
+  s = HostSchedule{};
+  const int L = (int)hp.tiles.size();
+  const int P = (L + 1) / 2;
+  const int64_t nb = (m + 255) / 256;
+  auto consecutive = [&](int t) {
+    if (t < 0) return false;
+    const TileMeta &tm = hp.tiles[(size_t)t];
+    if (tm.n_i != 128) return false;
+    for (int r = 1; r < 128; ++r)
+      if (hp.colids[(size_t)tm.col_off + r] != hp.colids[(size_t)tm.col_off] + r) return false;
+    return true;
+  };
+  std::vector<int32_t> flags((size_t)P);
+  for (int p = 0; p < P; ++p) {
+    const int t1 = 2 * p + 1 < L ? 2 * p + 1 : -1;
+    flags[(size_t)p] = (consecutive(2 * p) ? 1 : 0) | (consecutive(t1) ? 2 : 0);
+    s.has_tma_rows = s.has_tma_rows || flags[(size_t)p] != 0;
+  }
+  const int64_t n_units = nb * P;
+  if (n_units > INT32_MAX / 4) return fail(TW_ERR_UNSUPPORTED, "schedule too long");
+  const int C = (int)std::max<int64_t>(1, std::min<int64_t>(clusters, n_units));
+  // token-block-major order dealt round-robin: pairs running at the same
+  // time share their A^T token block in L2
+  std::vector<std::vector<int32_t>> per((size_t)C);
+  for (int64_t i = 0; i < n_units; ++i) {
+    const int64_t b = i / P, p = i % P;
+    const int t1 = 2 * (int)p + 1 < L ? 2 * (int)p + 1 : -1;
+    auto &v = per[(size_t)(i % C)];
+    v.insert(v.end(), {2 * (int32_t)p, t1, (int32_t)(b * 256), flags[(size_t)p]});
+  }
+  s.grid = 2 * C;
+  s.pair = true;
+  s.off.assign((size_t)C + 1, 0);
+  for (int c = 0; c < C; ++c) {
+    s.units.insert(s.units.end(), per[(size_t)c].begin(), per[(size_t)c].end());
+    s.off[(size_t)c + 1] = (int32_t)(s.units.size() / 4);
+  }
+  const int64_t Z = zero_rows ? (int64_t)hp.zero_rows.size() : 0;
+  s.zoff.assign((size_t)s.grid + 1, 0);
+  for (int c = 0; c < s.grid; ++c) s.zoff[(size_t)c + 1] = (int32_t)(Z * (c + 1) / s.grid);
+  s.soff.assign((size_t)s.grid + 1, 0);
+  return TW_OK;
+}
+
 }  // namespace tw

@@ -91,6 +91,23 @@ def _plan_args(tiles, col_range):
     return (k, n, g, int(c0), int(c1), col_off, col_ids, words, subs, sub_off)
 
 
+# TwPlan(dense_pad=None) packs a plan dense (K4) when its live tiles keep at
+# least this fraction of their rows (measured crossover).
+DENSE_PAD_MIN_DENSITY = float(os.environ.get("TW_B200_DENSE_PAD_MIN", "0.6"))
+
+
+def tile_density(k: int, col_off, words) -> float:
+    """Kept fraction of the live tiles' rows: sum k_i n_i / (K sum n_i) over
+    tiles with k_i > 0 (words = the packed row masks, one row of uint32 words
+    per tile)."""
+    w = np.asarray(words, dtype=np.uint32).reshape(len(col_off) - 1, -1)
+    k_i = np.unpackbits(w.view(np.uint8), axis=1).sum(axis=1).astype(np.int64)
+    n_i = np.diff(np.asarray(col_off, dtype=np.int64))
+    live = k_i > 0
+    den = int(k) * int(n_i[live].sum())
+    return float((k_i * n_i)[live].sum()) / den if den else 0.0
+
+
 class PackedPlan:
     """The packed image of a CompactTileSet (csrc/tw_pack.cpp): padded kept-K
     index lists, output column ids, the zero-row list (pruned columns and
@@ -199,12 +216,22 @@ class TwPlan(PackedPlan):
       "exact" -- the reference's own rounding sequence (fp32 multiply, fp32
                  add, ascending k) on CUDA cores with the fp32 weights
                  (TW_PLAN_F32_WEIGHTS): bit-identical to tilewise.gemm_tw.
-    `prep(a32)` produces the matching activation operand."""
+    `prep(a32)` produces the matching activation operand.
+
+    dense_pad (kernel choice, "bf16" plans of G <= 128): True packs every
+    live tile with ALL K rows, the pruned ones as zero weights
+    (TW_PLAN_DENSE_PAD), which runs on the CTA-pair kernel K4 (A^T by TMA
+    tiles, 256 x 256 per SM pair); False keeps the kept-row gather kernel K2;
+    None (default) picks K4 when the live tiles keep at least
+    DENSE_PAD_MIN_DENSITY of their rows -- the near-dense regime where gathering
+    the kept rows costs more than multiplying the pruned ones by zero.  Same
+    products either way (a pruned weight contributes 0 * a; non-finite
+    activations in a tile's pruned rows would give NaN, as in a dense GEMM)."""
 
     _create = "tw_plan_create_ex"
 
     def __init__(self, tiles: CompactTileSet, device=None, dtype=None, col_range=None, _arrays=None,
-                 precision: str = "bf16"):
+                 precision: str = "bf16", dense_pad=None):
         if torch is None:
             raise RuntimeError("torch is required for device plans")
         if precision not in PRECISIONS:
@@ -217,6 +244,9 @@ class TwPlan(PackedPlan):
         self.dtype = dtype
         self.precision = precision
         self._flags = {"bf16": 0, "fp32": _lib.TW_PLAN_SPLIT3, "exact": _lib.TW_PLAN_F32_WEIGHTS}[precision]
+        if dense_pad and precision != "bf16":
+            raise ValueError("dense_pad applies to precision='bf16' plans")
+        self._dense_pad = dense_pad if precision == "bf16" else False
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         super().__init__(tiles, "bf16" if dtype == torch.bfloat16 else "fp16", col_range, _arrays)
 
@@ -242,9 +272,19 @@ class TwPlan(PackedPlan):
         return cls(None, device=device, dtype=dtype, col_range=col_range, precision=precision,
                    _arrays=(int(k), int(n), int(g), col_off, col_ids, words, subs, sub_off))
 
-    def _build(self, *args):
+    def _build(self, handle, k, n, g, nt, col_off, col_ids, words, subs, sub_off, c0, c1):
+        pad = self._dense_pad
+        if pad is None:
+            pad = g <= 128 and tile_density(k, col_off, words) >= DENSE_PAD_MIN_DENSITY
+        if pad:
+            self._flags |= _lib.TW_PLAN_DENSE_PAD
         with torch.cuda.device(self.device):
-            super()._build(*args)
+            super()._build(handle, k, n, g, nt, col_off, col_ids, words, subs, sub_off, c0, c1)
+
+    @property
+    def dense_padded(self) -> bool:
+        """True when the plan was packed with TW_PLAN_DENSE_PAD (runs on K4)."""
+        return bool(self._flags & _lib.TW_PLAN_DENSE_PAD)
 
     # -------------------------------------------------------------- compute
     def _check_at(self, at):
