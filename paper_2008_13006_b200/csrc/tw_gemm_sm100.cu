@@ -268,6 +268,7 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
   constexpr int WROWS = NROWS / 8;                   // rows stored by each epilogue warp
   static_assert(T % 32 == 0 && CH % 8 == 0 && 32 % LPR == 0, "epilogue tiling");
   static_assert(NROWS * RT * (int)sizeof(S) <= 32768, "staging buffer");
+  constexpr int kBufFloats = NROWS * RT * (int)sizeof(S) / 4;  // the two pass buffers are back to back
   const int toks = nq * 64;
   const int n_pass = (toks + RT - 1) / RT;
   const int region = BN <= 128 ? 0 : h;
@@ -287,7 +288,7 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
   uint32_t v[32];
   load(0, 0, v);
   for (int p = 0; p < n_pass; ++p) {
-    S *buf = reinterpret_cast<S *>(sStage + (p & 1) * (32768 / 4));
+    S *buf = reinterpret_cast<S *>(sStage + (p & 1) * kBufFloats);
     const int tau = p * RT + tw0;
     if (warp_live && tau < toks) {
       uint4 *row = reinterpret_cast<uint4 *>(buf + col % NROWS * RT);
@@ -313,7 +314,7 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
         }
       }
     }
-    if (p == n_pass - 1) {  // every TMEM read of the unit is done: hand the accumulator back
+    if (p == n_pass - 1 && tempty != nullptr) {  // every TMEM read of the unit is done: hand the accumulator back
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty);
     }
@@ -396,12 +397,13 @@ __device__ __forceinline__ void trace_epi(const GemmArgs &a, int unit_i, int pas
     a.trace[(int64_t)gridDim.x * 192 + (int64_t)blockIdx.x * 32 + pass * 4 + slot] = (int64_t)clock64();
 }
 
-template <int BN, typename OutT, bool kTrace>
+template <int BN, typename OutT, bool kTrace, int kRowBytesIn = 0>
 __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out, uint8_t *sStg, uint32_t t_acc,
                                                 uint64_t *tempty, const TileMeta &t, int m0, int nq,
                                                 const int32_t *ucol, int q, int h, int e, int lane, int unit_i) {
   constexpr int kRows = BN <= 128 ? 128 : 256;
-  constexpr int kRowBytes = BN <= 128 ? 512 : 256;
+  // staged bytes per row and pass (K4 passes 256: half the staging)
+  constexpr int kRowBytes = kRowBytesIn ? kRowBytesIn : (BN <= 128 ? 512 : 256);
   constexpr int kStride = kRowBytes + 16;
   constexpr int kPassTok = kRowBytes / (int)sizeof(OutT);
   constexpr int kWarpTok = BN <= 128 ? kPassTok / 2 : kPassTok;  // tokens per warp per pass
@@ -486,12 +488,12 @@ __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out,
 // per lane) hit 8 distinct bank groups, so the 16-byte shared stores are
 // conflict-free.  Warp (q, h): rows 32q.., tokens h * pass/2 ..; lane 0 of
 // warps 0..3 issues box e of the pass.  Tokens >= M are clipped by the TMA.
-template <typename OutT, bool kTrace>
+template <typename OutT, bool kTrace, int kBoxes = 4>
 __device__ __forceinline__ void drain_unit_tma(const GemmArgs &args, uint8_t *sStg, uint32_t t_acc, uint64_t *tempty,
                                                const TileMeta &t, int m0, int nq, int row0, int q, int h, int e,
                                                int lane) {
   constexpr int kBoxTok = 128 / (int)sizeof(OutT);      // tokens per box row (128 B)
-  constexpr int kPassTok = 4 * kBoxTok;                  // 4 boxes (64 KB) per pass
+  constexpr int kPassTok = kBoxes * kBoxTok;             // kBoxes boxes (16 KB each) per pass
   constexpr int kChunks = 32 * (int)sizeof(OutT) / 16;  // 16-byte chunks per 32 tokens
   const int toks = nq * 64;
   const int n_pass = (toks + kPassTok - 1) / kPassTok;
@@ -533,7 +535,7 @@ __device__ __forceinline__ void drain_unit_tma(const GemmArgs &args, uint8_t *sS
     }
     ptx::fence_proxy_async_smem();  // the staging boxes are read by the TMA (async proxy)
     epi_sync();
-    if (lane == 0 && e < 4 && e * kBoxTok < pt && !(kTrace && (args.debug & 2))) {
+    if (lane == 0 && e < kBoxes && e * kBoxTok < pt && !(kTrace && (args.debug & 2))) {
       ptx::tma_store_2d(&args.tmap_out, sStg + e * 16384, m0 + ptok0 + e * kBoxTok, row0);
       ptx::bulk_commit();
     }
@@ -1008,10 +1010,15 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 // barrier), 1 MMA (leader only; commits multicast to both CTAs), 2..9
 // epilogue (each CTA drains its own TMEM: its tile's 128 rows x 256 tokens,
 // K2's drain functions), zero rows as in K2.
-constexpr int kPairStages = 4;
+#ifndef TW_PAIR_STAGES
+#define TW_PAIR_STAGES 5
+#endif
+constexpr int kPairStages = TW_PAIR_STAGES;
 constexpr int kPairThreads = 10 * 32;
 constexpr uint32_t kPairStageBytes = 32768;  // 16 KB weight block + 16 KB A^T half
-constexpr uint32_t kPairStagingBytes = 69632;
+// epilogue staging: 2 TMA boxes (32 KB) or 128 rows x 272 B (bulk row
+// stores) per pass -- half of K2's, for one more pipeline stage
+constexpr uint32_t kPairStagingBytes = 128 * 272;
 constexpr uint32_t kPairSmem = 1024 + kPairStages * kPairStageBytes + kPairStagingBytes + 2 * 128 * 4 + 256 + 8192;
 static_assert(kPairSmem <= 232448u, "K4 shared memory budget");
 
@@ -1155,10 +1162,16 @@ __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __
       epi_sync();
       const uint32_t t_acc = tmem_base + (uint32_t)(acc * 256);
       if (tile >= 0) {
-        if (args.tma_out && ((su.w >> rank) & 1))
-          drain_unit_tma<OutT, false>(args, sStage, t_acc, nullptr, t, su.z, 4, ucol[0], q, h, e, lane);
-        else
-          drain_unit_bulk<128, OutT, false>(args, out, sStage, t_acc, nullptr, t, su.z, 4, ucol, q, h, e, lane, 0);
+        if (args.tma_out && ((su.w >> rank) & 1)) {
+          drain_unit_tma<OutT, false, 2>(args, sStage, t_acc, nullptr, t, su.z, 4, ucol[0], q, h, e, lane);
+        } else if constexpr (sizeof(OutT) == 2) {
+          // scattered output rows: 16-byte LSU stores from the staging rows
+          // (K4's loads are all TMA, so the LSU is free -- unlike in K2)
+          drain_unit<128, OutT, OutT, 32, false, false>(args, out, reinterpret_cast<float *>(sStage), t_acc, nullptr, t,
+                                                       su.z, 4, ucol, q, h, e, lane, true);
+        } else {
+          drain_unit_bulk<128, OutT, false, 256>(args, out, sStage, t_acc, nullptr, t, su.z, 4, ucol, q, h, e, lane, 0);
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();

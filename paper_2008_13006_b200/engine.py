@@ -93,7 +93,7 @@ def _plan_args(tiles, col_range):
 
 # TwPlan(dense_pad=None) packs a plan dense (K4) when its live tiles keep at
 # least this fraction of their rows (measured crossover).
-DENSE_PAD_MIN_DENSITY = float(os.environ.get("TW_B200_DENSE_PAD_MIN", "0.6"))
+DENSE_PAD_MIN_DENSITY = float(os.environ.get("TW_B200_DENSE_PAD_MIN", "0.55"))
 
 
 def tile_density(k: int, col_off, words) -> float:
