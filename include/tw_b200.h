@@ -210,6 +210,9 @@ int tw_gemm_bias(const tw_plan *plan, const void *at, int64_t m, int64_t lda, vo
  * the previous work in the stream has completed (for isolated timing next to
  * library GEMMs, which are launched that way). */
 #define TW_GEMM_NO_PDL 4
+/* Run a K4-eligible plan (tw_plan_kernel) on K4 even when the layer does not
+ * fill a wave of CTA pairs (TwPlan(dense_pad=True): the caller's choice). */
+#define TW_GEMM_FORCE_PAIR 8
 int tw_gemm_ex(const tw_plan *plan, const void *at, int64_t m, int64_t lda, void *ct, int64_t ldc, int out_dtype,
                int flags, const float *bias, int relu, void *stream);
 
@@ -270,6 +273,12 @@ int tw_spmm_csc(const void *at, int at_dtype, int64_t k, int64_t m, int64_t lda,
 int tw_gemm_tew(const tw_plan *plan, const void *at, int64_t m, int64_t lda, const int32_t *col_ptr,
                 const int32_t *row_idx, const float *values, int64_t nnz, void *ct, int64_t ldc,
                 int out_dtype, void *stream);
+
+/* Which kernel tw_gemm(plan, M, out_dtype, accumulate = 0, 16-byte aligned
+ * output) runs on this device: 2 = K2 (kept-row gathers, one CTA per
+ * 128-column unit), 4 = K4 (CTA pairs; plans whose tiles keep every row in
+ * order, when the layer has at least one wave of 256 x 256 pair units). */
+int tw_plan_kernel(const tw_plan *plan, int64_t m, int out_dtype, int *kernel);
 
 /* Profiling hook: tw_gemm (accumulate = 0) that also records %globaltimer
  * stamps into the device buffer trace[grid * 8 units * 8 slots] (int64, ns;

@@ -56,6 +56,7 @@ SIGNATURES = {
     "tw_schedule_export": (_i32, [_p, _i64, _i32, _i32, _i32, _i32, _p, _pi64]),
     "tw_gemm": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _i32, _p]),
     "tw_gemm_traced": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _p, _p]),
+    "tw_plan_kernel": (_i32, [_p, _i64, _i32, _p]),
     "tw_gemm_bias": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _p, _i32, _p]),
     "tw_gemm_ex": (_i32, [_p, _p, _i64, _i64, _p, _i64, _i32, _i32, _p, _i32, _p]),
     "tw_gemm_peers": (_i32, [_p, _p, _i64, _i64, _p, _i32, _i64, _i32, _p]),

@@ -139,6 +139,15 @@ int pair_cluster_count(int out_dtype) {
   return n;
 }
 
+// K4 runs a pair_ok plan when the layer fills at least one wave of the
+// device's CTA pairs (smaller layers: K2's 128-column units spread wider).
+int pair_clusters_for(const tw_plan *p, int64_t m, int out_dtype, bool force = false) {
+  if (!p->pair_ok) return 0;
+  const int c = pair_cluster_count(out_dtype);
+  const int64_t units = (m + 255) / 256 * (int64_t)((p->host.tiles.size() + 1) / 2);
+  return (units >= c || force) ? c : 0;
+}
+
 // Static schedule for (M, output width, zero rows on/off), built once per
 // launch shape and cached on the plan (uploaded to the plan's device).
 int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, const tw_dev_schedule **out,
@@ -160,6 +169,9 @@ int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, c
   ds.has_contig = hs.has_contig;
   ds.has_tma_rows = hs.has_tma_rows;
   ds.pair = hs.pair;
+  ds.h_off = hs.off;
+  ds.h_soff = hs.soff;
+  ds.h_zoff = hs.zoff;
   std::vector<int4> units(hs.units.size() / 4);
   for (size_t i = 0; i < units.size(); ++i)
     units[i] = make_int4(hs.units[4 * i], hs.units[4 * i + 1], hs.units[4 * i + 2], hs.units[4 * i + 3]);
@@ -387,7 +399,7 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   int pair_clusters = 0;
   if (pair_env && p->pair_ok && !accum && n_peer == 0 && trace == nullptr && hp.a_rows == hp.k &&
       (reinterpret_cast<uintptr_t>(ct) & 15) == 0 && (ldc * ob) % 16 == 0 && (m * ob) % 16 == 0)
-    pair_clusters = pair_cluster_count(out_dtype);
+    pair_clusters = pair_clusters_for(p, m, out_dtype, (accumulate & TW_GEMM_FORCE_PAIR) != 0);
   if ((rc = get_schedule(p, m, ob, !accum && !keep_pruned, sms, &sched, pair_clusters))) return rc;
   GemmArgs a{};
   a.tiles = p->d_tiles;
@@ -463,6 +475,12 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
     if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed: " + std::to_string((int)r));
     a.tma_out = 1;
   }
+  if (sched->grid <= kParamCtas) {
+    a.cta_par = 1;
+    for (size_t i = 0; i < sched->h_off.size() && i <= (size_t)kParamCtas; ++i) a.cta_off[0][i] = sched->h_off[i];
+    for (size_t i = 0; i < sched->h_soff.size() && i <= (size_t)kParamCtas; ++i) a.cta_off[1][i] = sched->h_soff[i];
+    for (size_t i = 0; i < sched->h_zoff.size() && i <= (size_t)kParamCtas; ++i) a.cta_off[2][i] = sched->h_zoff[i];
+  }
   a.trace = trace;
   a.bias = bias;
   a.relu = relu;
@@ -481,6 +499,21 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   cudaError_t e = sched->pair ? launch_tw_pair_sm100(a, out_dtype, grid, reinterpret_cast<cudaStream_t>(stream))
                               : launch_tw_gemm_sm100(a, out_dtype, grid, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tw_gemm launch");
+  return TW_OK;
+}
+
+int tw_plan_kernel(const tw_plan *p, int64_t m, int out_dtype, int *kernel) {
+  clear_error();
+  if (!p || !kernel) return fail(TW_ERR_ARG, "null argument");
+  if (p->device < 0) return fail(TW_ERR_ARG, "host-only plan");
+  DeviceGuard guard(p->device);
+  if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice(plan device)");
+  const int ob = out_size(out_dtype);
+  static const bool pair_env = [] {
+    const char *e = std::getenv("TW_B200_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  *kernel = (pair_env && (m * ob) % 16 == 0 && pair_clusters_for(p, m, out_dtype) > 0) ? 4 : 2;
   return TW_OK;
 }
 

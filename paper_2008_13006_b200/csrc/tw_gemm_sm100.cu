@@ -542,6 +542,18 @@ __device__ __forceinline__ void drain_unit_tma(const GemmArgs &args, uint8_t *sS
   }
 }
 
+// Per-CTA schedule offsets: kernel parameters when the grid fits
+// (GemmArgs::cta_off), else the schedule's global arrays.
+__device__ __forceinline__ int sched_off_of(const GemmArgs &a, int i) {
+  return a.cta_par ? a.cta_off[0][i] : __ldg(a.sched_off + i);
+}
+__device__ __forceinline__ int stream_off_of(const GemmArgs &a, int i) {
+  return a.cta_par ? a.cta_off[1][i] : __ldg(a.stream_off + i);
+}
+__device__ __forceinline__ int zero_off_of(const GemmArgs &a, int i) {
+  return a.cta_par ? a.cta_off[2][i] : __ldg(a.zero_off + i);
+}
+
 // Profiling hook: globaltimer stamps per CTA and work unit (tw_gemm_traced).
 // Slots: 0 producer unit start, 1 producer unit issued, 2 MMA start, 3 MMA
 // committed, 4 epilogue started waiting, 5 accumulator ready, 6 unit stored.
@@ -595,11 +607,36 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int u_begin = __ldg(args.sched_off + blockIdx.x);
-  const int u_end = __ldg(args.sched_off + blockIdx.x + 1);
-  const int s_begin = __ldg(args.stream_off + blockIdx.x);
-  const int n_st = __ldg(args.stream_off + blockIdx.x + 1) - s_begin;
+  const int u_begin = sched_off_of(args, blockIdx.x);
+  const int u_end = sched_off_of(args, blockIdx.x + 1);
+  const int s_begin = stream_off_of(args, blockIdx.x);
+  const int n_st = stream_off_of(args, blockIdx.x + 1) - s_begin;
 
+  if (warp < kProducerWarps) {
+    // the first kIdxLook stages' row indices + records are requested before
+    // the prologue (barrier init, TMEM allocation, CTA barrier): their DRAM
+    // round trip overlaps it (one cp.async group per stage, as in the loop)
+    const int grp = warp / kGroupWarps, gw = warp % kGroupWarps;
+    const int my_st = n_st > grp ? (n_st - grp + kProducerGroups - 1) / kProducerGroups : 0;
+    int32_t *ring = sIdx + warp * (kIdxSlots * kSlotInts);
+    for (int k = 0; k < kIdxLook; ++k) {
+      if (k < my_st && lane <= kIdxLanes) {
+        const int32_t *src = args.stream + (int64_t)(s_begin + grp + k * kProducerGroups) * kIdxInts +
+                             (lane < kIdxLanes ? gw * kRowsPerWarp + lane * 4 : 64);
+        ptx::cp_async_16(ring + (k % kIdxSlots) * kSlotInts + lane * 4, src, 16);
+      }
+      ptx::cp_async_commit();
+    }
+  }
+  // the weight warp's first 32 stage records, likewise before the prologue
+  int w_pre[4] = {0, 0, 0, 0};
+  if (warp == kWWarp && lane < n_st) {
+    const int32_t *rec = args.stream + (int64_t)(s_begin + lane) * kIdxInts;
+    w_pre[0] = __ldg(rec + 64);
+    w_pre[1] = __ldg(rec + 65);
+    w_pre[2] = __ldg(rec + 66);
+    w_pre[3] = __ldg(rec);
+  }
   if (threadIdx.x == 0) {
     trace_evt<kTrace>(args, 7, 0);  // CTA start
     if constexpr (kTrace) args.trace[((int64_t)blockIdx.x * 8 + 7) * 8 + 2] = (int64_t)clock64();
@@ -656,10 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         ptx::cp_async_16(ring + (k % kIdxSlots) * kSlotInts + lane * 4, src, 16);
       }
     };
-    for (int k = 0; k < kIdxLook; ++k) {  // one cp.async group per prefetched stage
-      if (k < my_st) prefetch(k);
-      ptx::cp_async_commit();
-    }
+    // (the first kIdxLook stages were requested before the prologue, above)
     // A^T may be produced by the previous kernel in the stream (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     constexpr bool traced = kTrace;
@@ -850,8 +884,8 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     uint32_t phase = 0;
     for (int i0 = 0; i0 < n_st; i0 += 32) {
       // lane l: stage i0 + l's weight offset, flags, first token and first row
-      int woff_l = 0, z_l = 0, m0_l = 0, r0_l = 0;
-      if (i0 + lane < n_st) {
+      int woff_l = w_pre[0], m0_l = w_pre[1], z_l = w_pre[2], r0_l = w_pre[3];  // i0 = 0: loaded at CTA start
+      if (i0 > 0 && i0 + lane < n_st) {
         const int32_t *rec = args.stream + (int64_t)(s_begin + i0 + lane) * kIdxInts;
         woff_l = __ldg(rec + 64);
         m0_l = __ldg(rec + 65);
@@ -912,11 +946,11 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // producer's weight loads, and a burst of zero-row stores queued ahead
     // of them stalls the pipeline; the remainder is split over all 8 warps
     // once the CTA's last accumulator has been drained.
-    int zr = __ldg(args.zero_off + blockIdx.x);
+    int zr = zero_off_of(args, blockIdx.x);
     volatile int32_t *s_zdone = reinterpret_cast<volatile int32_t *>(tmem_holder + 1);
     // the output may be read / written by the previous kernel (PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int z1 = (args.accumulate || args.keep_pruned || dbg<kTrace>(args, 1)) ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
+    const int z1 = (args.accumulate || args.keep_pruned || dbg<kTrace>(args, 1)) ? 0 : zero_off_of(args, blockIdx.x + 1);
     uint32_t use[2] = {0, 0};  // drained halves per accumulator region
     OutT *out = reinterpret_cast<OutT *>(args.out);
     for (int j = u_begin; j < u_end; ++j) {
@@ -1042,8 +1076,8 @@ __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __
   const int lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_rank();
   const int cl = blockIdx.x >> 1;
-  const int u_begin = __ldg(args.sched_off + cl);
-  const int u_end = __ldg(args.sched_off + cl + 1);
+  const int u_begin = sched_off_of(args, cl);
+  const int u_end = sched_off_of(args, cl + 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -1138,8 +1172,8 @@ __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __
     const int q = warp & 3;  // TMEM lane quadrant of this warp
     const int h = e >> 2;
     const uint32_t tempty_lead = ptx::mapa(ptx::smem_u32(tempty), 0);
-    int zr = __ldg(args.zero_off + blockIdx.x);
-    const int z1 = args.keep_pruned ? 0 : __ldg(args.zero_off + blockIdx.x + 1);
+    int zr = zero_off_of(args, blockIdx.x);
+    const int z1 = args.keep_pruned ? 0 : zero_off_of(args, blockIdx.x + 1);
     volatile int32_t *s_zdone = reinterpret_cast<volatile int32_t *>(tmem_holder + 1);
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the output may be read / written by the previous kernel
     uint32_t use[2] = {0, 0};

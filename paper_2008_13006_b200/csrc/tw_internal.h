@@ -91,6 +91,8 @@ bool pair_eligible(const HostPlan &hp);
 // (off: clusters + 1); zero rows split evenly over the 2 * clusters CTAs.
 int build_pair_schedule(const HostPlan &hp, int64_t m, bool zero_rows, int clusters, HostSchedule &s);
 
+constexpr int kParamCtas = 160;
+
 // Kernel arguments of the persistent TW-GEMM (tw_gemm_sm100.cu).
 struct GemmArgs {
   const TileMeta *tiles;
@@ -127,6 +129,12 @@ struct GemmArgs {
                         // 128B swizzle; valid when tma_out != 0
   int32_t tma_out;
   CUtensorMap tmap_w;  // K4: the weight image as 2-D (128-byte rows), box 128 B x 128 rows, no swizzle
+  // per-CTA schedule offsets as kernel parameters (cta_par = 1, grids of up
+  // to kParamCtas CTAs): {sched_off, stream_off, zero_off}[i] without a
+  // dependent global load at CTA start (one DRAM round trip less before the
+  // first gather / weight load)
+  int32_t cta_par;
+  int32_t cta_off[3][kParamCtas + 1];
   int32_t debug;      // experiment knobs (TW_B200_DEBUG): bit0 skip zero rows, bit1 skip kept-row stores
 };
 
@@ -146,6 +154,7 @@ struct tw_dev_schedule {
   bool has_contig = false;
   bool has_tma_rows = false;
   bool pair = false;  // K4 schedule (grid = 2 x clusters)
+  std::vector<int32_t> h_off, h_soff, h_zoff;  // host copies (kernel-parameter offsets)
   int4 *units = nullptr;
   int32_t *off = nullptr;
   int32_t *zoff = nullptr;

@@ -278,6 +278,7 @@ class TwPlan(PackedPlan):
             pad = g <= 128 and tile_density(k, col_off, words) >= DENSE_PAD_MIN_DENSITY
         if pad:
             self._flags |= _lib.TW_PLAN_DENSE_PAD
+        self._build_args = (k, n, g, nt, col_off, col_ids, words, subs, sub_off, c0, c1)
         with torch.cuda.device(self.device):
             super()._build(handle, k, n, g, nt, col_off, col_ids, words, subs, sub_off, c0, c1)
 
@@ -334,7 +335,8 @@ class TwPlan(PackedPlan):
         if (accumulate or not write_pruned) and out is None:
             raise ValueError("accumulate=True / write_pruned=False need out")
         ct = self._out(m, out, out_dtype)
-        flags = (1 if accumulate else 0) | (0 if write_pruned else 2) | (0 if pdl else 4)
+        flags = (1 if accumulate else 0) | (0 if write_pruned else 2) | (0 if pdl else 4) | (
+            8 if self._dense_pad else 0)  # dense_pad=True: K4 whatever the layer size
         bias_ptr = None
         if bias is not None:
             if accumulate:
@@ -345,9 +347,39 @@ class TwPlan(PackedPlan):
             bias_ptr = bias.data_ptr()
         elif relu:
             raise ValueError("relu needs the bias epilogue (pass bias=zeros for a plain ReLU)")
-        _lib.call("tw_gemm_ex", self._h, at.data_ptr(), m, lda, ct.data_ptr(), ct.stride(0), _code(out_dtype),
+        plan = self._for_launch(m, out_dtype)
+        _lib.call("tw_gemm_ex", plan._h, at.data_ptr(), m, lda, ct.data_ptr(), ct.stride(0), _code(out_dtype),
                   flags, bias_ptr, 1 if relu else 0, _stream_ptr(stream, self.device))
         return ct
+
+    def kernel_for(self, m: int, out_dtype=None) -> int:
+        """Which kernel a gemm() of M tokens runs: 2 (K2, kept-row gathers)
+        or 4 (K4, CTA pairs) -- tw_plan_kernel."""
+        kern = ctypes.c_int(0)
+        with torch.cuda.device(self.device):
+            _lib.call("tw_plan_kernel", self._h, int(m), _code(out_dtype or torch.float32), ctypes.byref(kern))
+        return kern.value
+
+    def _for_launch(self, m: int, out_dtype):
+        """An auto-padded plan (dense_pad=None) whose layer is too small to
+        fill a wave of K4's CTA pairs launches its unpadded sibling on K2
+        instead (built once, on first use) -- K2 on a padded plan would gather
+        the pruned rows too."""
+        if self._dense_pad is not None or not self.dense_padded:
+            return self
+        kc = self.__dict__.setdefault("_kernel_cache", {})
+        key = (int(m), out_dtype)
+        if key not in kc:
+            kc[key] = self.kernel_for(m, out_dtype)
+        if kc[key] == 4:
+            return self
+        alt = self.__dict__.get("_unpadded")
+        if alt is None:
+            k, n, g, nt, col_off, col_ids, words, subs, sub_off, c0, c1 = self._build_args
+            alt = TwPlan(None, device=self.device, dtype=self.dtype, col_range=(c0, c1), precision=self.precision,
+                         dense_pad=False, _arrays=(k, n, g, col_off, col_ids, words, subs, sub_off))
+            self._unpadded = alt
+        return alt
 
     def gemm_exact(self, at32, out=None, stream=None):
         """Bit-exact CUDA-core variant (fp32 activations): mm_accum's exact

@@ -64,7 +64,7 @@ def ran_pair(names):
 
 @pytest.mark.parametrize("m,k,n", [(512, 256, 512), (1024, 768, 768), (320, 192, 256), (4096, 1024, 1024)])
 def test_dense_pattern_runs_on_pair_kernel(m, k, n):
-    plan, ct, want, _, names = run_case(m, k, n, 128, 0.0)
+    plan, ct, want, _, names = run_case(m, k, n, 128, 0.0, dense_pad=True)
     assert ran_pair(names), names
     assert rel_l2(ct, want) < 1e-5
 
@@ -81,6 +81,13 @@ def test_dense_pad_plan_vs_oracle(out_dtype, bar):
     assert plan.dense_padded and ran_pair(names), names
     assert np.all(ct[prc] == 0.0)
     assert rel_l2(ct, want) <= bar, rel_l2(ct, want)
+
+
+def test_dense_layer_at_full_wave_runs_k4_by_default():
+    # no dense_pad argument: a dense 4096 x 1024 x 4096 layer fills the CTA pairs
+    plan, ct, want, _, names = run_case(4096, 1024, 4096, 128, 0.0)
+    assert plan.kernel_for(4096) == 4 and ran_pair(names), names
+    assert rel_l2(ct, want) < 1e-5
 
 
 def test_dense_pad_off_keeps_gather_kernel():
@@ -100,7 +107,7 @@ def test_auto_choice_follows_density():
 @pytest.mark.parametrize("n", [128, 384, 640])
 def test_odd_tile_count(n):
     # the last CTA pair has one tile: the follower computes a copy and stores nothing
-    plan, ct, want, _, names = run_case(768, 256, n, 128, 0.0)
+    plan, ct, want, _, names = run_case(768, 256, n, 128, 0.0, dense_pad=True)
     assert ran_pair(names)
     assert rel_l2(ct, want) < 1e-5
 
@@ -108,7 +115,7 @@ def test_odd_tile_count(n):
 @pytest.mark.parametrize("m", [16, 136, 1000, 2056])
 def test_ragged_m(m):
     # tokens past M: zero-filled by the TMA loads, clipped by the TMA stores
-    plan, ct, want, _, names = run_case(m, 384, 512, 128, 0.0)
+    plan, ct, want, _, names = run_case(m, 384, 512, 128, 0.0, dense_pad=True)
     assert ran_pair(names)
     assert ct.shape == (512, m)
     assert rel_l2(ct, want) < 1e-5
@@ -139,7 +146,8 @@ def test_non_consecutive_tile_columns_and_dead_tiles():
 def test_bias_relu_epilogue(relu, out_dtype):
     n = 512
     bias = np.random.default_rng(2).standard_normal(n).astype(np.float32)
-    plan, ct, want, _, names = run_case(1024, 512, n, 128, 0.0, out_dtype=out_dtype, bias=bias, relu=relu)
+    plan, ct, want, _, names = run_case(1024, 512, n, 128, 0.0, out_dtype=out_dtype, bias=bias, relu=relu,
+                                        dense_pad=True)
     assert ran_pair(names)
     assert rel_l2(ct, want) <= (1e-3 if out_dtype == torch.float16 else 1e-5)
 
@@ -159,9 +167,10 @@ def test_back_to_back_launches_and_graph_replay():
     # PDL-chained launches and a captured graph over rotating outputs
     a, w, p = orc.bench_inputs(2048, 512, 1024, 128, 0.0, seed=4)
     pat = tw.TilePattern(p[0], p[1], p[2], tuple(tw.Tile(c, keep) for c, keep in p[3]))
-    plan = tw.TwPlan(tw.compact(tw.DenseMatrix.from_array(w), pat))
+    plan = tw.TwPlan(tw.compact(tw.DenseMatrix.from_array(w), pat), dense_pad=True)
     at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
-    ref = plan.gemm(at, out_dtype=torch.float16)
+    ref, names = kernels_of(lambda: plan.gemm(at, out_dtype=torch.float16))
+    assert ran_pair(names)
     outs = [torch.empty_like(ref) for _ in range(4)]
     for i in range(20):
         plan.gemm(at, out=outs[i % 4], out_dtype=torch.float16)
@@ -178,3 +187,15 @@ def test_back_to_back_launches_and_graph_replay():
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o, ref)
+
+
+def test_small_auto_padded_layer_launches_unpadded_plan_on_k2():
+    # C1 (1024^3 @ 50 %, 71 % of rows kept) is auto-padded, but its 12 pair
+    # units fill 12 of 74 CTA pairs: gemm() runs the unpadded sibling on K2
+    plan, ct, want, prc, names = run_case(1024, 1024, 1024, 128, 0.5)
+    assert plan.dense_padded
+    assert plan.kernel_for(1024) == 2 and not ran_pair(names), names
+    assert np.all(ct[prc] == 0.0)
+    assert rel_l2(ct, want) < 1e-5
+    # the same plan at a large M fills the pairs
+    assert plan.kernel_for(16384) == 4
