@@ -76,6 +76,18 @@ def load_peaks():
     return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
+def load_peaks_sustained() -> float:
+    """Sustained bf16 TF/s (cuBLAS back to back for seconds, at the power
+    cap): the tensor roofline for a kernel timed after bench.py's soak."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        if "bf16_tflops_sustained" in d:
+            return float(d["bf16_tflops_sustained"])
+    return load_peaks()[1]
+
+
 def resolve_workload(args, world: int) -> str:
     """--workload, else the BASELINE config for this GPU count: configs[1]
     (BERT-base FC1, 1 x B200) at N = 1, configs[4] (BERT-large FC1 at 75%,
@@ -424,12 +436,28 @@ def run_ours(args):
     bytes_alg = algorithmic_bytes(info, m, out_bytes) + (12 * csc_host.nnz if csc_host is not None else 0)
     achieved = bytes_alg / (ms * 1e-3) / 1e9
     traffic, traffic_detail = read_traffic(wl, args.out_dtype)
+    # which kernel ran: K2 (kept-row gathers; HBM/L2-bound) or K4 (CTA
+    # pairs on a dense / dense-padded plan; tensor-bound, timed after the
+    # soak at the board power cap -> the SUSTAINED bf16 peak)
+    if dcsc is None:
+        kern = plans[0]._for_launch(m, out_dt).kernel_for(m, out_dt)
+    else:  # gemm_tew runs the merged plan (built on the first call)
+        mp = plans[0].__dict__.get("_tew_plans", {}).get(dcsc)
+        kern = mp._for_launch(m, out_dt).kernel_for(m, out_dt) if mp is not None else 2
+    kept_tf = kept_flops / (ms * 1e-3) / 1e12
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic, "traffic_detail": traffic_detail,
                 "peak_kind": peak_kind,
-                "kernel": "tw_gemm_sm100_kernel", "algorithmic_bytes_per_launch": bytes_alg,
-                "kept_tflops": kept_flops / (ms * 1e-3) / 1e12,
-                "tensor_frac_of_bf16_peak": kept_flops / (ms * 1e-3) / 1e12 / tc_peak}
+                "kernel": "tw_gemm_sm100_kernel" if kern == 2 else "tw_pair_sm100_kernel",
+                "algorithmic_bytes_per_launch": bytes_alg,
+                "kept_tflops": kept_tf,
+                "tensor_frac_of_bf16_peak": kept_tf / tc_peak}
+    if kern == 4:
+        tc_sus = load_peaks_sustained()
+        roofline.update({"bound": "tensor", "achieved": kept_tf, "peak": tc_sus, "unit": "TFLOP/s",
+                         "frac": kept_tf / tc_sus, "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json)",
+                         "hbm_gbs": achieved, "hbm_frac": achieved / hbm_peak,
+                         "algorithmic_flops_per_launch": kept_flops})
 
     result = {}
     if rank == 0:

@@ -82,7 +82,7 @@ def merge(args):
         with open(csv_path) as f:
             lines = [ln for ln in f if ln.startswith('"')]
         for row in csv.DictReader(lines):
-            if "tw_gemm" not in row.get("Kernel Name", ""):
+            if "tw_gemm" not in row.get("Kernel Name", "") and "tw_pair" not in row.get("Kernel Name", ""):
                 continue
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(row.get("Metric Unit", "byte"), 1)
             per.setdefault(row["ID"], {})[row["Metric Name"]] = _num(row["Metric Value"]) * scale
