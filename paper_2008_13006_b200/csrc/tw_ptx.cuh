@@ -212,8 +212,13 @@ __device__ __forceinline__ uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
   return r;
 }
+// arrive on a barrier of a CTA of the cluster (default .release.cta
+// semantics, as CUTLASS's ClusterBarrier::arrive: a .cluster-scope release
+// would wait for every outstanding global store of the thread first; the
+// TMEM reads it publishes are ordered by tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
