@@ -144,8 +144,25 @@ int pair_cluster_count(int out_dtype) {
 int pair_clusters_for(const tw_plan *p, int64_t m, int out_dtype, bool force = false) {
   if (!p->pair_ok) return 0;
   const int c = pair_cluster_count(out_dtype);
-  const int64_t units = (m + 255) / 256 * (int64_t)((p->host.tiles.size() + 1) / 2);
-  return (units >= c || force) ? c : 0;
+  if (c <= 0) return 0;
+  if (force) return c;
+  // Stage-makespan model of both kernels (B200 measurements):
+  // a K4 stage (2 x 128 x 256 x 64 MACs per pair) ~0.44 us, every pair runs
+  // ceil(units / pairs) units of ceil(K / 64) stages; a K2 stage (128 x 256
+  // tokens x 64 kept rows) ~0.75 us, a 128-token tail stage ~0.62 us, the
+  // CTAs run the unpadded plan's ceil(kbar / 64) stages per unit.  K4 also
+  // needs half a wave of pairs (tiny layers: K2's units spread wider).
+  const HostPlan &hp = p->host;
+  const int64_t L = (int64_t)hp.tiles.size();
+  const int64_t blocks = (m + 255) / 256;
+  const int64_t u4 = blocks * ((L + 1) / 2);
+  if (2 * u4 < c) return 0;
+  const double t4 = 0.44 * (double)((u4 + c - 1) / c) * (double)((hp.k + 63) / 64);
+  const int64_t kbar = L > 0 ? (hp.kept_rows_live + L - 1) / L : hp.k;
+  const int64_t u2 = blocks * L, sms = 2 * (int64_t)c;
+  const double waves2 = (double)(u2 / sms) * 0.75 + (u2 % sms == 0 ? 0.0 : (u2 % sms <= sms / 2 ? 0.62 : 0.75));
+  const double t2 = waves2 * (double)((kbar + 63) / 64);
+  return t4 < t2 ? c : 0;
 }
 
 // Static schedule for (M, output width, zero rows on/off), built once per

@@ -1044,27 +1044,30 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 // barrier), 1 MMA (leader only; commits multicast to both CTAs), 2..9
 // epilogue (each CTA drains its own TMEM: its tile's 128 rows x 256 tokens,
 // K2's drain functions), zero rows as in K2.
-#ifndef TW_PAIR_STAGES
-#define TW_PAIR_STAGES 5
-#endif
-constexpr int kPairStages = TW_PAIR_STAGES;
 constexpr int kPairThreads = 10 * 32;
 constexpr uint32_t kPairStageBytes = 32768;  // 16 KB weight block + 16 KB A^T half
-// epilogue staging: 2 TMA boxes (32 KB) or 128 rows x 272 B (bulk row
-// stores) per pass -- half of K2's, for one more pipeline stage
-constexpr uint32_t kPairStagingBytes = 128 * 272;
-constexpr uint32_t kPairSmem = 1024 + kPairStages * kPairStageBytes + kPairStagingBytes + 2 * 128 * 4 + 256 + 8192;
-static_assert(kPairSmem <= 232448u, "K4 shared memory budget");
+// 16-bit output: 5 stages and half of K2's staging (2 TMA boxes, or 2 x 16 KB
+// LSU-path buffers, per pass); fp32 output: 4 stages and K2's full staging
+// (twice the output bytes per token)
+template <typename OutT>
+struct PairCfg {
+  static constexpr int kStages = sizeof(OutT) == 2 ? 5 : 4;
+  static constexpr uint32_t kStagingBytes = sizeof(OutT) == 2 ? 128 * 272 : 69632;
+  static constexpr int kTmaBoxes = sizeof(OutT) == 2 ? 2 : 4;
+  static constexpr uint32_t kSmem = 1024 + kStages * kPairStageBytes + kStagingBytes + 2 * 128 * 4 + 256 + 8192;
+  static_assert(kSmem <= 232448u, "K4 shared memory budget");
+};
 
 template <typename OutT>
 __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __grid_constant__ GemmArgs args) {
-  constexpr int S = kPairStages;
+  using PC = PairCfg<OutT>;
+  constexpr int S = PC::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sW = smem;                        // S x 16 KB weight blocks (K-major SW128, host-swizzled)
   uint8_t *sA = smem + S * 16384;            // S x 16 KB A^T halves (2 blocks of 64 tokens, SW128)
   uint8_t *sStage = sA + S * 16384;          // epilogue staging (1 KB aligned)
-  int32_t *sCol = reinterpret_cast<int32_t *>(sStage + kPairStagingBytes);
+  int32_t *sCol = reinterpret_cast<int32_t *>(sStage + PC::kStagingBytes);
   uint64_t *full = reinterpret_cast<uint64_t *>(sCol + 2 * 128);
   uint64_t *empty = full + S;
   uint64_t *tfull = empty + S;
@@ -1197,14 +1200,15 @@ __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __
       const uint32_t t_acc = tmem_base + (uint32_t)(acc * 256);
       if (tile >= 0) {
         if (args.tma_out && ((su.w >> rank) & 1)) {
-          drain_unit_tma<OutT, false, 2>(args, sStage, t_acc, nullptr, t, su.z, 4, ucol[0], q, h, e, lane);
+          drain_unit_tma<OutT, false, PC::kTmaBoxes>(args, sStage, t_acc, nullptr, t, su.z, 4, ucol[0], q, h, e, lane);
         } else if constexpr (sizeof(OutT) == 2) {
           // scattered output rows: 16-byte LSU stores from the staging rows
           // (K4's loads are all TMA, so the LSU is free -- unlike in K2)
           drain_unit<128, OutT, OutT, 32, false, false>(args, out, reinterpret_cast<float *>(sStage), t_acc, nullptr, t,
                                                        su.z, 4, ucol, q, h, e, lane, true);
         } else {
-          drain_unit_bulk<128, OutT, false, 256>(args, out, sStage, t_acc, nullptr, t, su.z, 4, ucol, q, h, e, lane, 0);
+          drain_unit<128, OutT, float, 32, false, false>(args, out, reinterpret_cast<float *>(sStage), t_acc, nullptr, t,
+                                                        su.z, 4, ucol, q, h, e, lane, true);
         }
       }
       ptx::tc_fence_before();
@@ -1231,7 +1235,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __
 template <typename OutT>
 cudaError_t launch_pair(const GemmArgs &args, int grid, cudaStream_t stream) {
   auto kern = tw_pair_sm100_kernel<OutT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairCfg<OutT>::kSmem);
   if (e != cudaSuccess) return e;
   static const bool pdl = [] {
     const char *v = std::getenv("TW_B200_PDL");
@@ -1240,7 +1244,7 @@ cudaError_t launch_pair(const GemmArgs &args, int grid, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kPairThreads);
-  cfg.dynamicSmemBytes = kPairSmem;
+  cfg.dynamicSmemBytes = PairCfg<OutT>::kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1259,11 +1263,12 @@ cudaError_t launch_pair(const GemmArgs &args, int grid, cudaStream_t stream) {
 template <typename OutT>
 int pair_clusters_of() {
   auto kern = tw_pair_sm100_kernel<OutT>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem) != cudaSuccess) return 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PairCfg<OutT>::kSmem) != cudaSuccess)
+    return 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2);
   cfg.blockDim = dim3(kPairThreads);
-  cfg.dynamicSmemBytes = kPairSmem;
+  cfg.dynamicSmemBytes = PairCfg<OutT>::kSmem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;

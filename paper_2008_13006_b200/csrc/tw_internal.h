@@ -54,6 +54,7 @@ struct HostPlan {
   std::vector<float> w32;             // TW_PLAN_F32_WEIGHTS: fp32 weights, per live tile nkb*64 x 128 (k-major)
   std::vector<int64_t> w32_off;       // per live tile offset into w32 (elements)
   int64_t kept_elems = 0, union_k = 0, sum_k = 0, sum_n = 0;
+  int64_t kept_rows_live = 0;  // sum of the live tiles' own kept rows (before TW_PLAN_DENSE_PAD)
 };
 
 // Static work schedule of one launch shape (plan, M, output width): CTA c

@@ -202,6 +202,7 @@ int build_host_plan(int64_t k, int64_t n, int64_t g, int64_t n_tiles, const int6
       for (int64_t kk = 0; kk < ktile; ++kk)
         for (int64_t j = 0; j < n_i; ++j) w[kk * 128 + j] = sub[(L.j0 + j) * ktile + kk];
     }
+    hp.kept_rows_live += L.k_i;
     hp.kept_elems += L.k_i * n_i;  // the reference's kept elements (FLOP count), not the split's 3x
     hp.sum_k += kx;
     hp.sum_n += n_i;

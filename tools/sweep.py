@@ -131,6 +131,12 @@ def run_row(name, m, k, n, s, delta, reps, hbm_peak):
         if od == "fp32":
             ct_slice = outs[0][:, : min(m, 1024)].float().cpu().numpy()
         del outs
+    # which kernel the (auto) plan runs at this M: 2 = K2 gathers, 4 = K4 CTA pairs
+    if csc is None:
+        res["kernel"] = plan._for_launch(m, torch.float16).kernel_for(m, torch.float16)
+    else:
+        mp = plan.__dict__.get("_tew_plans", {}).get(csc)
+        res["kernel"] = mp._for_launch(m, torch.float16).kernel_for(m, torch.float16) if mp is not None else 2
     # parity on a token slice
     ms = min(m, 1024)
     at32 = at[:, :ms].float().cpu().numpy()
@@ -180,16 +186,16 @@ def main():
         print(json.dumps(res), flush=True)
     with open(args.out + ".json", "w") as f:
         json.dump(results, f, indent=1)
-    lines = ["| row | M | K | N | elem. sparsity | TW fp32 µs | TW fp16 µs | cuBLAS bf16 µs | fp16 speedup | "
-             "fp32 GB/s (frac) | dense-eq TFLOPS (fp32) | rel-L2 |", "|" + "---|" * 12]
+    lines = ["| row | M | K | N | elem. sparsity | kernel | TW fp32 µs | TW fp16 µs | cuBLAS bf16 µs | fp16 speedup | "
+             "fp32 GB/s (frac) | dense-eq TFLOPS (fp32) | rel-L2 |", "|" + "---|" * 13]
     for r in results:
         cub = r.get("us_cublas_bf16")
         lines.append(
-            f"| {r['row']} | {r['m']} | {r['k']} | {r['n']} | {r['element_sparsity']:.3f} | {r['us_fp32']:.1f} | "
+            f"| {r['row']} | {r['m']} | {r['k']} | {r['n']} | {r['element_sparsity']:.3f} | K{r['kernel']} | {r['us_fp32']:.1f} | "
             f"{r['us_fp16']:.1f} | {cub:.1f} | {r['speedup_fp16_vs_cublas_bf16']:.2f}x | "
             f"{r['gbs_fp32']:.0f} ({r['hbm_frac_fp32']:.2f}) | {r['tflops_dense_fp32']:.0f} | {r['rel_l2']:.1e} |"
             if cub else
-            f"| {r['row']} | {r['m']} | {r['k']} | {r['n']} | {r['element_sparsity']:.3f} | {r['us_fp32']:.1f} | "
+            f"| {r['row']} | {r['m']} | {r['k']} | {r['n']} | {r['element_sparsity']:.3f} | K{r['kernel']} | {r['us_fp32']:.1f} | "
             f"{r['us_fp16']:.1f} | — | — | {r['gbs_fp32']:.0f} ({r['hbm_frac_fp32']:.2f}) | "
             f"{r['tflops_dense_fp32']:.0f} | {r['rel_l2']:.1e} |")
     with open(args.out + ".md", "w") as f:
