@@ -86,8 +86,13 @@ constexpr int kEpiBarrier = 1;  // named barrier id for the epilogue warps
 // cp.async while issuing stage i: no register ever waits on an index load.
 constexpr int kIdxInts = 68;
 constexpr int kSlotInts = kRowsPerWarp + 4;  // this warp's row indices + the 4-int record
-constexpr int kIdxSlots = 6;  // per warp, in the warp's own stage numbering
-constexpr int kIdxLook = 3;
+// Stage i + 1's indices are read into registers at the end of stage i,
+// right behind stage i's cp.async issue, so their MIO-queue latency overlaps
+// the next empty-slot wait instead of sitting at the head of every stage;
+// that needs the stream kIdxLook = 4 stages ahead and kIdxSlots - kIdxLook >=
+// kStages (the MMA warp reads each stage's record from the ring too).
+constexpr int kIdxSlots = 7;  // per warp, in the warp's own stage numbering
+constexpr int kIdxLook = 4;
 
 template <int BN>
 struct Cfg {
@@ -700,21 +705,34 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     // (tracing) which producer thread records per-stage cycles: warp 0 (it
     // also issues the weight TMA) or, with debug bit 65536, warp 1
     const int tr_thread = dbg<kTrace>(args, 65536) ? 32 : 0;
+    // this warp's 16 row indices + the record of a stage, ring -> registers
+    int4 rec_n = make_int4(0, 0, 0, 0);
+    int rows_n[kRowsPerWarp];
+    auto load_slot = [&](int li) {
+      const int32_t *slot = ring + (li % kIdxSlots) * kSlotInts;
+      rec_n = *reinterpret_cast<const int4 *>(slot + kRowsPerWarp);
+#pragma unroll
+      for (int v4 = 0; v4 < kRowsPerWarp / 4; ++v4) {
+        const int4 r4 = reinterpret_cast<const int4 *>(slot)[v4];
+        rows_n[4 * v4] = r4.x; rows_n[4 * v4 + 1] = r4.y; rows_n[4 * v4 + 2] = r4.z; rows_n[4 * v4 + 3] = r4.w;
+      }
+    };
+    if (my_st > 0) {
+      ptx::cp_async_wait_group<kIdxLook - 1>();  // stage 0's indices: the oldest of kIdxLook groups
+      __syncwarp();
+      load_slot(0);
+    }
     for (int li = 0; li < my_st; ++li) {
       const int i = grp + li * kProducerGroups;  // global stage
       const int stage = i % C::kStages;
       const uint32_t phase = (uint32_t)(i / C::kStages) & 1u;
-      const int32_t *slot = ring + (li % kIdxSlots) * kSlotInts;
       const long long c0 = traced ? clock64() : 0;  // SM-clock reads only when tracing
       // 4096 (experiment, needs 4 = no MMA): no back-pressure from the consumer
       // the first kStages slots start free: skip the (already complete) wait
       if (i >= C::kStages && !dbg<kTrace>(args, 4096)) ptx::mbar_wait(&empty[stage], phase ^ 1);
       const long long c1 = traced ? clock64() : 0;  // SM-clock reads only when tracing
-      // stage i's indices were the (kIdxLook)-th most recent group
-      ptx::cp_async_wait_group<kIdxLook - 1>();
-      __syncwarp();
       const long long c2 = traced ? clock64() : 0;  // SM-clock reads only when tracing
-      const int4 rec = *reinterpret_cast<const int4 *>(slot + kRowsPerWarp);
+      const int4 rec = rec_n;  // read at the end of the previous stage
       if (threadIdx.x == 0 && (rec.w & (1 << 16))) trace_evt<kTrace>(args, rec.w & 0xffff, 0);
       const int nq = rec.z & 0xf;           // 64-token quarters in this unit
       const bool active = chunk < nq * 8;   // this lane's 8 tokens are in the unit
@@ -727,10 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       // load issued after a cp.async waits for it in the same (MIO) pipe
       int rows[kRowsPerWarp];
 #pragma unroll
-      for (int v4 = 0; v4 < kRowsPerWarp / 4; ++v4) {
-        const int4 r4 = reinterpret_cast<const int4 *>(slot)[v4];
-        rows[4 * v4] = r4.x; rows[4 * v4 + 1] = r4.y; rows[4 * v4 + 2] = r4.z; rows[4 * v4 + 3] = r4.w;
-      }
+      for (int r = 0; r < kRowsPerWarp; ++r) rows[r] = rows_n[r];
       if (dbg<kTrace>(args, 8192)) {  // experiment: synthetic rows (random, in range) instead of the kept lists
 #pragma unroll
         for (int r = 0; r < kRowsPerWarp; ++r) rows[r] = ((gw * kRowsPerWarp + r) * 389 + i * 13 + blockIdx.x * 7) % 768;
@@ -794,6 +809,14 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       if (li + kIdxLook < my_st) prefetch(li + kIdxLook);
       ptx::cp_async_mbar_arrive_noinc(&full[stage]);  // also covers the prefetch
       ptx::cp_async_commit();
+      if (li + 1 < my_st) {
+        // the next stage's indices, queued right behind this stage's gathers:
+        // their group is now kIdxLook - 2 deep (it rode with stage li - 3,
+        // whose data the next empty wait needs anyway)
+        ptx::cp_async_wait_group<kIdxLook - 2>();
+        __syncwarp();
+        load_slot(li + 1);
+      }
       if (threadIdx.x == 0) trace_stage<kTrace>(args, i, 0);
       if (kTrace && threadIdx.x == tr_thread && i < 32) {
         const long long c3 = clock64();
