@@ -47,6 +47,8 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INCLUDE, "tw_b200.h"))
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
+    # (experiments) extra nvcc flags, e.g. -DTW_K2_STAGES=2; clear _build/ to rebuild
+    common += os.environ.get("TW_B200_NVCC_FLAGS", "").split()
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)

@@ -466,7 +466,7 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
     if (!enc) return fail(TW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {64, (cuuint64_t)(hp.wimg.size() / 128)};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {64, 128};
+    cuuint32_t box[2] = {64, (cuuint32_t)hp.wrows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&a.tmap_w, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->d_wimg, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

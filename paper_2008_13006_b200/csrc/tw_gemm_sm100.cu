@@ -112,9 +112,13 @@ struct Cfg {
                                      kProducerWarps * kIdxSlots * kSlotInts * 4 + kZeroBytes;
   // as many 64-k pipeline stages as fit next to the epilogue buffers (4 for
   // G <= 128): bytes in flight per SM set the gather throughput
+#ifdef TW_K2_STAGES  // (experiment) a shallower pipeline
+  static constexpr int kStages = TW_K2_STAGES;
+#else
   static constexpr int kStages = (int)((232448u - kFixed) / (kABytes + kBBytes)) > 4
                                      ? 4
                                      : (int)((232448u - kFixed) / (kABytes + kBBytes));
+#endif
   static constexpr uint32_t kSmem = kFixed + kStages * (kABytes + kBBytes);
   static_assert(kStages >= 3, "pipeline too shallow");
   static_assert(kSmem <= 232448u, "shared memory budget");
@@ -1140,10 +1144,12 @@ __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __
         const int tok = su.z + (int)rank * 128;
         for (int kb = 0; kb < t.nkb; ++kb, ++n) {
           if (n >= S) ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 4u * 16384u);
+          // both CTAs' weight blocks (wrows x 128 B; rows past wrows hold stale
+          // data that only reaches TMEM lanes >= n_i, never stored) + A^T halves
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2u * ((uint32_t)args.wbytes + 16384u));
           const uint32_t bar = full_lead + (uint32_t)stage * 8u;
           ptx::tma_load_2d_pair(sW + stage * 16384, &args.tmap_w, bar, 0,
-                                (int32_t)((t.w_off + (int64_t)kb * 16384) >> 7), keep);
+                                (int32_t)((t.w_off + (int64_t)kb * args.wbytes) >> 7), keep);
           ptx::tma_load_2d_pair(sA + stage * 16384, &args.tmap_at, bar, tok, kb * 64, keep);
           ptx::tma_load_2d_pair(sA + stage * 16384 + 8192, &args.tmap_at, bar, tok + 64, kb * 64, keep);
           if (++stage == S) { stage = 0; phase ^= 1; }

@@ -84,7 +84,7 @@ struct HostSchedule {
 int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows, int sms, int tb,
                    HostSchedule &s);
 // K4 (CTA-pair kernel): every live tile keeps all K rows in order (a dense
-// pattern or TW_PLAN_DENSE_PAD) with 128-row weight blocks.
+// pattern or TW_PLAN_DENSE_PAD) with weight blocks of at most 128 rows.
 bool pair_eligible(const HostPlan &hp);
 // K4 schedule: units {tile of CTA rank 0, tile of rank 1 (-1: none), first
 // token, consecutive-rows flags (bit r: rank r's tile owns 128 consecutive

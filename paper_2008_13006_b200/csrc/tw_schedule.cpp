@@ -275,7 +275,9 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
 }
 
 bool pair_eligible(const HostPlan &hp) {
-  if (hp.tiles.empty() || (hp.flags & TW_PLAN_SPLIT3) || hp.block_n != 128 || hp.wrows != 128) return false;
+  // (weight blocks of wrows <= 128 rows: a shard's or a narrow layer's tiles;
+  // the A operand rows past wrows are never stored)
+  if (hp.tiles.empty() || (hp.flags & TW_PLAN_SPLIT3) || hp.block_n != 128 || hp.wrows > 128) return false;
   for (const TileMeta &t : hp.tiles) {
     if (t.k_i != hp.k) return false;
     const int32_t *kx = &hp.kidx[(size_t)t.kidx_off];

@@ -199,3 +199,82 @@ def test_small_auto_padded_layer_launches_unpadded_plan_on_k2():
     assert rel_l2(ct, want) < 1e-5
     # the same plan at a large M fills the pairs
     assert plan.kernel_for(16384) == 4
+
+
+def test_column_range_shard_of_a_padded_plan():
+    # the N-sharded unit: a shard [c0, c1) cuts tiles (n_i < 128, scattered
+    # rows) -- K4 stores them through the LSU path; rows re-based to 0
+    a, w, p = orc.bench_inputs(2048, 512, 1024, 128, 0.3, seed=11)
+    pat = tw.TilePattern(p[0], p[1], p[2], tuple(tw.Tile(c, keep) for c, keep in p[3]))
+    ts = tw.compact(tw.DenseMatrix.from_array(w), pat)
+    at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), 512, 1024),
+                          threads=orc.max_threads())
+    for c0, c1 in ((0, 512), (100, 900), (777, 1024)):
+        plan = tw.TwPlan(ts, col_range=(c0, c1), dense_pad=True)
+        ct, names = kernels_of(lambda: plan.gemm(at, out_dtype=torch.float16))
+        assert ran_pair(names)
+        assert rel_l2(ct.float().cpu().numpy(), want[c0:c1]) <= 1e-3
+
+
+def test_resident_output_keep_pruned():
+    # write_pruned=False: the pruned rows of a reused buffer keep their value
+    plan, ct, want, prc, names = run_case(2048, 512, 1024, 128, 0.3, dense_pad=True)
+    a, w, p = orc.bench_inputs(2048, 512, 1024, 128, 0.3, seed=3)
+    at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
+    out = torch.full((1024, 2048), 7.0, dtype=torch.float32, device="cuda")
+    plan.gemm(at, out=out, write_pruned=False)
+    got = out.cpu().numpy()
+    kept = np.setdiff1d(np.arange(1024), prc)
+    assert np.all(got[prc] == 7.0)
+    assert rel_l2(got[kept], want[kept]) < 1e-5
+
+
+def test_fp16_operands():
+    a, w, p = orc.bench_inputs(1024, 512, 1024, 128, 0.1, seed=5)
+    pat = tw.TilePattern(p[0], p[1], p[2], tuple(tw.Tile(c, keep) for c, keep in p[3]))
+    ts = tw.compact(tw.DenseMatrix.from_array(w), pat)
+    plan = tw.TwPlan(ts, dtype=torch.float16, dense_pad=True)
+    at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.float16)
+    ct, names = kernels_of(lambda: plan.gemm(at))
+    assert ran_pair(names)
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), 512, 1024),
+                          threads=orc.max_threads())
+    # fp16 operands round A and W differently from the bf16-rounded oracle inputs
+    assert rel_l2(ct.cpu().numpy(), want) <= 1e-3
+
+
+def test_layer_chain_through_near_dense_layers():
+    # TwMlp with near-dense layers (auto-padded, K4 at this size) feeding each
+    # layer's C^T in as the next A^T, against the oracle layer by layer
+    rng = np.random.default_rng(8)
+    m, dims = 8192, [512, 1024, 512]
+    pats, ws, bs = [], [], []
+    for i in range(2):
+        k, n = dims[i], dims[i + 1]
+        _, w, p = orc.bench_inputs(8, k, n, 128, 0.15, seed=20 + i)
+        pats.append(p)
+        ws.append(w)
+        bs.append(rng.standard_normal(n).astype(np.float32))
+    layers = []
+    for p, w, b in zip(pats, ws, bs):
+        pat = tw.TilePattern(p[0], p[1], p[2], tuple(tw.Tile(c, keep) for c, keep in p[3]))
+        plan = tw.TwPlan(tw.compact(tw.DenseMatrix.from_array(w), pat))
+        assert plan.dense_padded
+        layers.append((plan, torch.from_numpy(b).cuda()))
+    x = orc.bf16_round(rng.standard_normal((m, dims[0])).astype(np.float32))
+    at = tw.prep_activations(torch.from_numpy(x).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
+    ref = np.ascontiguousarray(x.T)
+    for li, ((plan, b), p, w) in enumerate(zip(layers, pats, ws)):
+        last = li == len(layers) - 1
+        ct, names = kernels_of(lambda: plan.gemm(at, out_dtype=torch.float32 if last else torch.bfloat16,
+                                                 bias=b, relu=not last))
+        assert ran_pair(names)
+        want = orc.gemm_tw_ct(ref, orc.PackedTiles(orc.compact(w, p), w.shape[0], w.shape[1]),
+                              threads=orc.max_threads()) + bs[li][:, None]
+        if not last:
+            want = np.maximum(want, 0)
+        got = ct.float().cpu().numpy()
+        assert rel_l2(got, want) <= (5e-3 if not last else 1e-3), (li, rel_l2(got, want))
+        at = ct  # C^T of this layer is A^T of the next
+        ref = got.astype(np.float32)  # the oracle continues from the GPU's rounded activations
