@@ -11,7 +11,7 @@
 
 namespace tw {
 int tokens_per_unit(int block_n);
-cudaError_t launch_tw_gemm_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream);
+cudaError_t launch_tw_gemm_sm100(const GemmArgs &args, int out_dtype, int grid, int tb, cudaStream_t stream);
 cudaError_t launch_tw_pair_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream);
 int pair_clusters_max(int out_dtype);
 cudaError_t launch_prep(const float *a, int64_t m, int64_t k, int layout, void *at, int64_t ldat, int out_dtype,
@@ -186,6 +186,13 @@ int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, c
   ds.has_contig = hs.has_contig;
   ds.has_tma_rows = hs.has_tma_rows;
   ds.pair = hs.pair;
+  // the K2 instantiation: the narrowest unit width that holds every piece
+  // (narrow kernels run deeper pipelines; TW_B200_NARROW=0 keeps the wide one)
+  static const bool narrow = [] {
+    const char *e = std::getenv("TW_B200_NARROW");
+    return !(e && e[0] == '0');
+  }();
+  ds.tb = narrow ? std::max(64, 64 * hs.max_nq) : 256;
   ds.h_off = hs.off;
   ds.h_soff = hs.soff;
   ds.h_zoff = hs.zoff;
@@ -514,7 +521,7 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   }
   const int grid = sched->grid;
   cudaError_t e = sched->pair ? launch_tw_pair_sm100(a, out_dtype, grid, reinterpret_cast<cudaStream_t>(stream))
-                              : launch_tw_gemm_sm100(a, out_dtype, grid, reinterpret_cast<cudaStream_t>(stream));
+                              : launch_tw_gemm_sm100(a, out_dtype, grid, sched->tb, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tw_gemm launch");
   return TW_OK;
 }

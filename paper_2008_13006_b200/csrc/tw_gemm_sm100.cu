@@ -89,38 +89,58 @@ constexpr int kSlotInts = kRowsPerWarp + 4;  // this warp's row indices + the 4-
 // Stage i + 1's indices are read into registers at the end of stage i,
 // right behind stage i's cp.async issue, so their MIO-queue latency overlaps
 // the next empty-slot wait instead of sitting at the head of every stage;
-// that needs the stream kIdxLook = 4 stages ahead and kIdxSlots - kIdxLook >=
-// kStages (the MMA warp reads each stage's record from the ring too).
-constexpr int kIdxSlots = 7;  // per warp, in the warp's own stage numbering
-constexpr int kIdxLook = 4;
+// that needs the stream kIdxLook stages ahead and kIdxSlots - kIdxLook >=
+// kStages (the MMA warp reads each stage's record from the ring too).  The
+// loop's cp.async.wait_group<kIdxLook - 2> bounds the stages whose gathers
+// are in flight to kIdxLook - 1, so a deeper pipeline needs a longer look.
 
-template <int BN>
+// Pipeline configuration per (BN = tile width, TB = max tokens per unit).
+// TB = 256 (BN = 128) / 128 (BN = 256) are the wide configurations; the
+// narrow ones (BN = 128, TB = 64 | 128) serve schedules whose pieces are all
+// at most TB tokens (small-M layers such as C1 / C2b, whose per-CTA chain is
+// a few 64-k stages of one narrow piece): a stage costs 8 | 16 KB of A^T
+// instead of 32 KB, so more stages fit, and a latency-bound chain of small
+// stages runs that many deep.
+template <int BN, int TB_ = (BN <= 128 ? 256 : 128)>
 struct Cfg {
-  static constexpr int TB = BN <= 128 ? 256 : 128;           // max tokens per unit
-  static constexpr uint32_t kABytes = TB * kBlockK * 2;       // gathered A^T rows per stage: 32 KB | 16 KB
+  static constexpr int TB = TB_;                              // max tokens per unit
+  static constexpr bool kWide = TB == (BN <= 128 ? 256 : 128);
+  static constexpr uint32_t kABytes = TB * kBlockK * 2;       // gathered A^T rows per stage: 32 KB | 16 KB | 8 KB
   static constexpr uint32_t kBBytes = BN * 128;               // weight block per stage: 16 KB | 32 KB
   static constexpr uint32_t kAccCols = 256;                   // TMEM columns per accumulator
   static constexpr uint32_t kTmemCols = 2 * kAccCols;
   // epilogue staging: a whole unit of 16-bit output (BN <= 128: 128 rows x
   // 512 B, BN = 256: 256 rows x 256 B) with 16 B of padding per row, so the
   // 32 rows of one tcgen05.ld land in distinct bank groups; drain_unit's two
-  // 32 KB LSU-path buffers alias the same region
-  static constexpr uint32_t kStagingBytes = 69632;
+  // 32 KB LSU-path buffers alias the same region.  TB = 64: one 64-token
+  // pass (fp32: 128 rows x 272 B bulk staging, one 32 KB LSU buffer)
+  static constexpr uint32_t kStagingBytes = TB >= 128 ? 69632 : 34816;
+  static constexpr int kIdxLook = TB >= 128 && kWide ? 4 : (TB >= 128 ? 5 : 8);
+  static constexpr int kStagesMax = TB >= 128 && kWide ? 4 : (TB >= 128 ? 4 : 7);
+  static constexpr int kIdxSlots = kWide ? 7 : kIdxLook + kStagesMax;  // per warp, in the warp's own stage numbering
   static constexpr uint32_t kColBytes = 2 * BN * 4;                     // col-id table, double buffered
   static constexpr uint32_t kZeroBytes = 8192;  // zero source block for TMA zero-row stores
   static constexpr uint32_t kFixed = 1024 /*align slack*/ + kStagingBytes + kColBytes + 256 /*barriers*/ +
                                      kProducerWarps * kIdxSlots * kSlotInts * 4 + kZeroBytes;
-  // as many 64-k pipeline stages as fit next to the epilogue buffers (4 for
-  // G <= 128): bytes in flight per SM set the gather throughput
+  // as many 64-k pipeline stages as fit next to the epilogue buffers (3 for
+  // the wide G <= 128 configuration)
 #ifdef TW_K2_STAGES  // (experiment) a shallower pipeline
   static constexpr int kStages = TW_K2_STAGES;
 #else
-  static constexpr int kStages = (int)((232448u - kFixed) / (kABytes + kBBytes)) > 4
-                                     ? 4
+  static constexpr int kStages = (int)((232448u - kFixed) / (kABytes + kBBytes)) > kStagesMax
+                                     ? kStagesMax
                                      : (int)((232448u - kFixed) / (kABytes + kBBytes));
 #endif
   static constexpr uint32_t kSmem = kFixed + kStages * (kABytes + kBBytes);
-  static_assert(kStages >= 3, "pipeline too shallow");
+  // epilogue pass widths: bulk-store staging row bytes (0 = the wide
+  // default) and TMA tensor-store boxes per pass
+  template <typename OutT>
+  __host__ __device__ static constexpr int bulk_row_bytes() { return kWide ? 0 : TB * (int)sizeof(OutT); }
+  template <typename OutT>
+  __host__ __device__ static constexpr int tma_boxes() { return kWide ? 4 : TB * (int)sizeof(OutT) / 128; }
+  static_assert(kStages >= 2, "pipeline too shallow");
+  static_assert(kIdxSlots - kIdxLook >= kStages, "index ring shorter than the pipeline");
+  static_assert(2 * kStages + 5 <= 32, "barrier block");
   static_assert(kSmem <= 232448u, "shared memory budget");
 };
 
@@ -592,9 +612,10 @@ __device__ __forceinline__ void trace_stage(const GemmArgs &a, int s, int slot) 
   }
 }
 
-template <int BN, typename OutT, bool kPeer, bool kTrace>
+template <int BN, int TBK, typename OutT, bool kPeer, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid_constant__ GemmArgs args) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, TBK>;
+  constexpr int kIdxSlots = C::kIdxSlots, kIdxLook = C::kIdxLook;
   constexpr int TB = C::TB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB alignment (SW128 atoms) by pointer arithmetic on the __shared__
@@ -792,14 +813,20 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
 #pragma unroll
         for (int it = 0; it < kRowsPerWarp / kRowsPerInst; ++it) {
           const int rl = it * kRowsPerInst + rsub;
-          const int row = kRowsPerInst == 1 ? rows[it] : (rsub ? rows[it * kRowsPerInst + 1] : rows[it * kRowsPerInst]);
+          int row = rows[it * kRowsPerInst];
+#pragma unroll
+          for (int x = 1; x < kRowsPerInst; ++x)
+            if (rsub == x) row = rows[it * kRowsPerInst + x];
           if (active) ptx::cp_async_16_full(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16), lane_base + (int64_t)row * pitch);
         }
       } else {
 #pragma unroll
         for (int it = 0; it < kRowsPerWarp / kRowsPerInst; ++it) {
           const int rl = it * kRowsPerInst + rsub;  // row within this warp's kRowsPerWarp
-          const int row = kRowsPerInst == 1 ? rows[it] : (rsub ? rows[it * kRowsPerInst + 1] : rows[it * kRowsPerInst]);
+          int row = rows[it * kRowsPerInst];
+#pragma unroll
+          for (int x = 1; x < kRowsPerInst; ++x)
+            if (rsub == x) row = rows[it * kRowsPerInst + x];
           const uint32_t nbytes = row >= 0 ? src_bytes_m : 0u;
           if (active)
             ptx::cp_async_16(a_warp + rl * 128 + ((cc ^ (rl & 7)) * 16),
@@ -1014,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
       } else if (BN <= 128 && !kPeer && args.tma_out && (su.w & 2) && !dbg<kTrace>(args, 524288)) {
         // 128 consecutive output rows: 2-D TMA tensor stores (every unit,
         // the CTA's last included: 4 store instructions per pass)
-        drain_unit_tma<OutT, kTrace>(args, reinterpret_cast<uint8_t *>(sStage), tmem_base + (uint32_t)(acc * C::kAccCols),
+        drain_unit_tma<OutT, kTrace, C::template tma_boxes<OutT>()>(args, reinterpret_cast<uint8_t *>(sStage), tmem_base + (uint32_t)(acc * C::kAccCols),
                                      &tempty[acc], t, m0, nq, ucol[0], q, h, e, lane);
       } else if (!kPeer && !args.accumulate && bulk_ok && !dbg<kTrace>(args, 131072) &&
                  (j + 1 < u_end || dbg<kTrace>(args, 262144))) {
@@ -1023,14 +1050,14 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         // and one bulk copy per row piece costs ~30 cycles of the TMA unit
         // (~2 us for a 128 x 256-token unit), which the 16-byte stores beat
         // TMA bulk-store epilogue (bit 131072: force the LSU path, experiment)
-        drain_unit_bulk<BN, OutT, kTrace>(args, out, reinterpret_cast<uint8_t *>(sStage),
+        drain_unit_bulk<BN, OutT, kTrace, C::template bulk_row_bytes<OutT>()>(args, out, reinterpret_cast<uint8_t *>(sStage),
                                           tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t, m0, nq, ucol, q,
                                           h, e, lane, j - u_begin);
       } else if (args.accumulate || sizeof(OutT) == 4) {
         drain_unit<BN, OutT, float, 32, kPeer, kTrace>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
                                          m0, nq, ucol, q, h, e, lane, vec);
       } else if constexpr (sizeof(OutT) == 2) {
-        drain_unit<BN, OutT, OutT, 64, kPeer, kTrace>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
+        drain_unit<BN, OutT, OutT, (TBK >= 128 ? 64 : 32), kPeer, kTrace>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
                                         m0, nq, ucol, q, h, e, lane, vec);
       }
       if (e == 0 && lane == 0) trace_evt<kTrace>(args, j - u_begin, 6);
@@ -1310,10 +1337,10 @@ int pair_clusters_of() {
   return n;
 }
 
-template <int BN, typename OutT, bool kPeer, bool kTrace>
+template <int BN, int TB, typename OutT, bool kPeer, bool kTrace>
 cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
-  auto kern = tw_gemm_sm100_kernel<BN, OutT, kPeer, kTrace>;
-  const int smem = (int)Cfg<BN>::kSmem;
+  auto kern = tw_gemm_sm100_kernel<BN, TB, OutT, kPeer, kTrace>;
+  const int smem = (int)Cfg<BN, TB>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   // programmatic dependent launch (TW_B200_PDL=0 disables): the next grid's
@@ -1337,20 +1364,25 @@ cudaError_t launch_bn(const GemmArgs &args, int grid, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// BN = 128 tiles: the kernel's unit width TB is the schedule's widest piece
+// (64 / 128 / 256 tokens, narrow_tb()); BN = 256 tiles: 128.
+template <typename OutT, bool kPeer, bool kTrace>
+cudaError_t launch_tb(const GemmArgs &args, int grid, int tb, cudaStream_t stream) {
+  if (args.block_n > 128) return launch_bn<256, 128, OutT, kPeer, kTrace>(args, grid, stream);
+  if (tb <= 64) return launch_bn<128, 64, OutT, kPeer, kTrace>(args, grid, stream);
+  if (tb <= 128) return launch_bn<128, 128, OutT, kPeer, kTrace>(args, grid, stream);
+  return launch_bn<128, 256, OutT, kPeer, kTrace>(args, grid, stream);
+}
+
 template <typename OutT>
-cudaError_t launch_out(const GemmArgs &args, int grid, cudaStream_t stream) {
+cudaError_t launch_out(const GemmArgs &args, int grid, int tb, cudaStream_t stream) {
   // peer-store variant (tw_gemm_peers) only when there are replicas: the
   // extra store loop costs the plain kernel registers and ~1 us at C2a;
   // the traced variant (timeline stamps + experiment knobs) only for
   // tw_gemm_traced -- the production instantiation carries neither
-  if (args.n_peer > 0)
-    return args.block_n <= 128 ? launch_bn<128, OutT, true, false>(args, grid, stream)
-                               : launch_bn<256, OutT, true, false>(args, grid, stream);
-  if (args.trace != nullptr)
-    return args.block_n <= 128 ? launch_bn<128, OutT, false, true>(args, grid, stream)
-                               : launch_bn<256, OutT, false, true>(args, grid, stream);
-  return args.block_n <= 128 ? launch_bn<128, OutT, false, false>(args, grid, stream)
-                             : launch_bn<256, OutT, false, false>(args, grid, stream);
+  if (args.n_peer > 0) return launch_tb<OutT, true, false>(args, grid, tb, stream);
+  if (args.trace != nullptr) return launch_tb<OutT, false, true>(args, grid, tb, stream);
+  return launch_tb<OutT, false, false>(args, grid, tb, stream);
 }
 
 }  // namespace
@@ -1375,11 +1407,11 @@ int pair_clusters_max(int out_dtype) {
   return 0;
 }
 
-cudaError_t launch_tw_gemm_sm100(const GemmArgs &args, int out_dtype, int grid, cudaStream_t stream) {
+cudaError_t launch_tw_gemm_sm100(const GemmArgs &args, int out_dtype, int grid, int tb, cudaStream_t stream) {
   switch (out_dtype) {
-    case TW_F32: return launch_out<float>(args, grid, stream);
-    case TW_BF16: return launch_out<__nv_bfloat16>(args, grid, stream);
-    case TW_F16: return launch_out<__half>(args, grid, stream);
+    case TW_F32: return launch_out<float>(args, grid, tb, stream);
+    case TW_BF16: return launch_out<__nv_bfloat16>(args, grid, tb, stream);
+    case TW_F16: return launch_out<__half>(args, grid, tb, stream);
   }
   return cudaErrorInvalidValue;
 }

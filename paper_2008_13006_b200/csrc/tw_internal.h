@@ -79,6 +79,7 @@ struct HostSchedule {
   bool has_contig = false;     // some stage's 64 kept rows are consecutive (TMA tile loads, record bit 12)
   bool has_tma_rows = false;   // some unit's tile has 128 consecutive output rows (unit flag bit 1)
   bool pair = false;           // K4 (CTA-pair) schedule: off is per cluster, no stage stream
+  int max_nq = 0;              // widest half (64-token quarters) of any unit
   double makespan_ns = 0, mean_ns = 0;
 };
 int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows, int sms, int tb,
@@ -155,6 +156,7 @@ struct tw_dev_schedule {
   bool has_contig = false;
   bool has_tma_rows = false;
   bool pair = false;  // K4 schedule (grid = 2 x clusters)
+  int tb = 256;       // K2 unit width the launch instantiates (64 / 128 / 256 tokens)
   std::vector<int32_t> h_off, h_soff, h_zoff;  // host copies (kernel-parameter offsets)
   int4 *units = nullptr;
   int32_t *off = nullptr;

@@ -229,8 +229,10 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
       bool rows_consecutive = t.n_i == 128 && hp.block_n == 128;
       for (int r = 1; r < t.n_i && rows_consecutive; ++r)
         rows_consecutive = hp.colids[(size_t)t.col_off + r] == hp.colids[(size_t)t.col_off] + r;
-      for (int h = 0; h < nh; ++h)
+      for (int h = 0; h < nh; ++h) {
         s.units.insert(s.units.end(), {u.tile, hm0[h], hq[h], reg[h] | (rows_consecutive ? 2 : 0)});
+        s.max_nq = std::max(s.max_nq, hq[h]);
+      }
       s.has_tma_rows = s.has_tma_rows || rows_consecutive;
       for (int kb = 0; kb < t.nkb; ++kb) {
         const int64_t woff = t.w_off + kb * wbytes;
