@@ -62,6 +62,8 @@ WORKLOADS = {
     "VGG_conv3_2": (200704, 2304, 256, 128, 0.75, "VGG-16 conv3_2 im2col b64: M=200704 K=2304 N=256, 75% TW"),
     "VGG_conv4_2": (50176, 4608, 512, 128, 0.50, "VGG-16 conv4_2 im2col b64: M=50176 K=4608 N=512, 50% TW"),
 }
+if os.environ.get("TW_BENCH_M"):  # (experiments only) override M of every workload
+    WORKLOADS = {k: (int(os.environ["TW_BENCH_M"]),) + v[1:] for k, v in WORKLOADS.items()}
 # TEW workloads: overlay fraction delta (tew_overlay_magnitude, test_engine.py:216-230 recipe)
 TEW_DELTA = {"C4": 0.015}
 L2_BYTES = 126 * 2**20

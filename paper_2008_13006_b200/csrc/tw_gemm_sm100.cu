@@ -284,10 +284,18 @@ __device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int la
 //     and, in every pass, tokens [p*2T + h*T, +T): a staged row holds 2T
 //     contiguous tokens.
 //   BN == 256: region h (columns 128h..128h+127); each warp all tokens.
+// (tracing) SM-clock stamps of the bulk epilogue of a CTA's first unit:
+// trace[grid*192 + cta*32 + pass*4 + {0 staging free, 1 staged, 2 synced, 3 issued}]
+template <bool kTrace>
+__device__ __forceinline__ void trace_epi(const GemmArgs &a, int unit_i, int pass, int slot, int e, int lane) {
+  if (kTrace && unit_i == 0 && pass < 8 && e == 0 && lane == 0)
+    a.trace[(int64_t)gridDim.x * 192 + (int64_t)blockIdx.x * 32 + pass * 4 + slot] = (int64_t)clock64();
+}
+
 template <int BN, typename OutT, typename S, int T, bool kPeer, bool kTrace>
 __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, float *sStage, uint32_t t_acc,
                                            uint64_t *tempty, const TileMeta &t, int m0, int nq, const int32_t *ucol,
-                                           int q, int h, int e, int lane, bool vec) {
+                                           int q, int h, int e, int lane, bool vec, int unit_i = -1) {
   constexpr int RT = BN <= 128 ? 2 * T : T;          // tokens per staged row per pass
   constexpr int NROWS = BN <= 128 ? 128 : 256;       // staged rows (tile columns)
   constexpr int CH = RT * (int)sizeof(S) / 16;       // 16-byte chunks per staged row
@@ -315,8 +323,10 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
     if (warp_live && tau < toks) ptx::tmem_ld_32x32b_x32(t_base + (uint32_t)tau, v);
   };
   uint32_t v[32];
+  trace_epi<kTrace>(args, unit_i, 7, 0, e, lane);  // (tracing) entry
   load(0, 0, v);
   for (int p = 0; p < n_pass; ++p) {
+    trace_epi<kTrace>(args, unit_i, p, 0, e, lane);
     S *buf = reinterpret_cast<S *>(sStage + (p & 1) * kBufFloats);
     const int tau = p * RT + tw0;
     if (warp_live && tau < toks) {
@@ -347,7 +357,9 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty);
     }
+    trace_epi<kTrace>(args, unit_i, p, 1, e, lane);
     epi_sync();  // publishes buf[p & 1]; the stores of pass p - 1 (same buffer at p + 1) are done
+    trace_epi<kTrace>(args, unit_i, p, 2, e, lane);
     if (p + 1 < n_pass) load(p + 1, 0, v);
     // store phase: warp e stores staged rows e*WROWS .. +WROWS, RPI rows per instruction
     const int lrow = lane / LPR, piece = lane % LPR;
@@ -402,6 +414,7 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
         }
       }
     }
+    trace_epi<kTrace>(args, unit_i, p, 3, e, lane);
   }
 }
 
@@ -418,14 +431,6 @@ __device__ __forceinline__ void drain_unit(const GemmArgs &args, OutT *out, floa
 //   BN <= 128: 128 rows x 512 B per pass (16-bit: the whole 256-token unit;
 //     fp32: 128 tokens); warp (q, h): rows 32q.., tokens h * pass/2 ..
 //   BN == 256: 256 rows x 256 B per pass; warp (q, h): rows 128h + 32q..
-// (tracing) SM-clock stamps of the bulk epilogue of a CTA's first unit:
-// trace[grid*192 + cta*32 + pass*4 + {0 staging free, 1 staged, 2 synced, 3 issued}]
-template <bool kTrace>
-__device__ __forceinline__ void trace_epi(const GemmArgs &a, int unit_i, int pass, int slot, int e, int lane) {
-  if (kTrace && unit_i == 0 && pass < 8 && e == 0 && lane == 0)
-    a.trace[(int64_t)gridDim.x * 192 + (int64_t)blockIdx.x * 32 + pass * 4 + slot] = (int64_t)clock64();
-}
-
 template <int BN, typename OutT, bool kTrace, int kRowBytesIn = 0>
 __device__ __forceinline__ void drain_unit_bulk(const GemmArgs &args, OutT *out, uint8_t *sStg, uint32_t t_acc,
                                                 uint64_t *tempty, const TileMeta &t, int m0, int nq,
@@ -1055,10 +1060,10 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
                                           h, e, lane, j - u_begin);
       } else if (args.accumulate || sizeof(OutT) == 4) {
         drain_unit<BN, OutT, float, 32, kPeer, kTrace>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
-                                         m0, nq, ucol, q, h, e, lane, vec);
+                                         m0, nq, ucol, q, h, e, lane, vec, j - u_begin);
       } else if constexpr (sizeof(OutT) == 2) {
         drain_unit<BN, OutT, OutT, (TBK >= 128 ? 64 : 32), kPeer, kTrace>(args, out, sStage, tmem_base + (uint32_t)(acc * C::kAccCols), &tempty[acc], t,
-                                        m0, nq, ucol, q, h, e, lane, vec);
+                                        m0, nq, ucol, q, h, e, lane, vec, j - u_begin);
       }
       if (e == 0 && lane == 0) trace_evt<kTrace>(args, j - u_begin, 6);
       ++use[acc];

@@ -155,7 +155,12 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
     const char *e = std::getenv("TW_B200_PAIRS");
     return e && e[0] == '1';
   }();
-  const int qh = tb / 64;
+  // (experiment) TW_B200_MAXQ = widest piece in 64-token quarters
+  static const int maxq = [] {
+    const char *e = std::getenv("TW_B200_MAXQ");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int qh = maxq > 0 ? std::min(tb / 64, maxq) : tb / 64;
   std::vector<std::vector<Unit>> cands{pieces(qh)};
   const std::vector<Unit> base = cands[0];  // a copy: cands grows below
   auto split_tail = [&](size_t from, int P) {
