@@ -516,3 +516,45 @@ def test_mlp_cuda_graph_replay_matches_eager():
         got = graphed(at)
         torch.cuda.synchronize()
         assert torch.equal(got, eager)
+
+
+_NARROW_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2008_13006_b200 as tw
+from oracle import oracle as orc
+m, k, n, s, seed, dt = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), float(sys.argv[5]), int(sys.argv[6]), sys.argv[7]
+a, w, p = orc.bench_inputs(m, k, n, 128, s, seed=seed)
+pat = tw.TilePattern(k, n, 128, tuple(tw.Tile(c, keep) for c, keep in p[3]))
+plan = tw.TwPlan(tw.compact(tw.DenseMatrix.from_array(w), pat), dense_pad=False)
+at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
+ct = plan.gemm(at, out_dtype={"fp32": torch.float32, "fp16": torch.float16}[dt])
+np.save(sys.argv[8], ct.float().cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("m,k,n,s,dt", [(512, 768, 768, 0.75, "fp16"), (1024, 1024, 1024, 0.5, "fp32"),
+                                        (2048, 768, 768, 0.75, "fp16"), (320, 1024, 512, 0.6, "fp32")])
+def test_narrow_unit_width_kernels_match_wide(tmp_path, m, k, n, s, dt):
+    """Small-M layers whose schedule pieces are all <= 64 / 128 tokens launch
+    the narrow K2 instantiations (TB = 64 / 128, deeper pipelines).  They do
+    the same per-element fp32 accumulation in the same k order as the wide
+    (TB = 256) kernel, so the outputs are bit-identical; the wide run is
+    forced with TW_B200_NARROW=0 in a fresh process (the switch is read once).
+    Both are also held to the oracle."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for narrow in ("1", "0"):
+        f = str(tmp_path / f"ct_{narrow}.npy")
+        env = dict(os.environ, TW_B200_NARROW=narrow)
+        subprocess.run([sys.executable, "-c", _NARROW_SCRIPT, root, str(m), str(k), str(n), str(s), "21", dt, f],
+                       check=True, env=env, timeout=300)
+        outs[narrow] = np.load(f)
+    assert np.array_equal(outs["1"], outs["0"]), "narrow and wide K2 instantiations differ"
+    a, w, p = orc.bench_inputs(m, k, n, 128, s, seed=21)
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), k, n))
+    assert rel_l2(outs["1"], want) <= RTOL
+    assert np.all(outs["1"][orc.pruned_columns(p)] == 0.0)
