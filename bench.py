@@ -69,6 +69,41 @@ TEW_DELTA = {"C4": 0.015}
 L2_BYTES = 126 * 2**20
 
 
+def pcie_floor(torch, h2d_bytes, d2h_bytes, reps=5):
+    """The e2e call's copy floor on this box: plain 1-D pinned copies of the
+    same byte counts, each direction alone (median of reps), and both at once
+    on two streams (PCIe is full duplex).  Context for e2e, not part of it."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    h_in = torch.empty(h2d_bytes // 4, dtype=torch.float32, pin_memory=True)
+    h_out = torch.empty(d2h_bytes // 4, dtype=torch.float32, pin_memory=True)
+    d_in = torch.empty(h2d_bytes // 4, dtype=torch.float32, device=dev)
+    d_out = torch.empty(d2h_bytes // 4, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    def both():
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+
+    t_in = timed(lambda: d_in.copy_(h_in, non_blocking=True))
+    t_out = timed(lambda: h_out.copy_(d_out, non_blocking=True))
+    t_both = timed(both)
+    return {"h2d_ms": t_in * 1e3, "d2h_ms": t_out * 1e3, "both_ms": t_both * 1e3,
+            "h2d_gbs": h2d_bytes / t_in / 1e9, "d2h_gbs": d2h_bytes / t_out / 1e9,
+            "note": "1-D pinned copies of the e2e byte counts on this box: the e2e call's PCIe floor"}
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -563,7 +598,8 @@ def run_ours(args):
                              "h2d_bytes_per_step": 4 * m * k, "d2h_bytes_per_step": 4 * m * n_total,
                              "api": (f"paper_2008_13006_b200.{'gemm_tew' if csc_host is not None else 'gemm_tw'}"
                                      "(DenseMatrix fp32 host, CompactTileSet[, CscMatrix]) -> "
-                                     "COL_MAJOR DenseMatrix (pinned host buffers)")}
+                                     "COL_MAJOR DenseMatrix (pinned host buffers)"),
+                             "pcie": pcie_floor(_t, 4 * m * k, 4 * m * n_total)}
 
         # ---- CPU baseline: reference algorithm (oracle C port) on host cores
         if world == 1 and not args.no_cpu:
