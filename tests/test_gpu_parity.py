@@ -528,14 +528,26 @@ a, w, p = orc.bench_inputs(m, k, n, 128, s, seed=seed)
 pat = tw.TilePattern(k, n, 128, tuple(tw.Tile(c, keep) for c, keep in p[3]))
 plan = tw.TwPlan(tw.compact(tw.DenseMatrix.from_array(w), pat), dense_pad=False)
 at = tw.prep_activations(torch.from_numpy(a).cuda(), tw.Layout.ROW_MAJOR, torch.bfloat16)
-ct = plan.gemm(at, out_dtype={"fp32": torch.float32, "fp16": torch.float16}[dt])
+odt = {"fp32": torch.float32, "fp16": torch.float16}[dt]
+mode = sys.argv[9]
+if mode == "bias":
+    bias = torch.from_numpy(np.random.default_rng(5).standard_normal(n).astype(np.float32)).cuda()
+    ct = plan.gemm(at, out_dtype=odt, bias=bias, relu=True)
+elif mode == "accum":
+    base = torch.from_numpy(np.random.default_rng(6).standard_normal((n, m)).astype(np.float32)).cuda().to(odt)
+    ct = base.clone()
+    plan.gemm(at, out=ct, out_dtype=odt, accumulate=True)
+else:
+    ct = plan.gemm(at, out_dtype=odt)
 np.save(sys.argv[8], ct.float().cpu().numpy())
 """
 
 
-@pytest.mark.parametrize("m,k,n,s,dt", [(512, 768, 768, 0.75, "fp16"), (1024, 1024, 1024, 0.5, "fp32"),
-                                        (2048, 768, 768, 0.75, "fp16"), (320, 1024, 512, 0.6, "fp32")])
-def test_narrow_unit_width_kernels_match_wide(tmp_path, m, k, n, s, dt):
+@pytest.mark.parametrize("m,k,n,s,dt,mode", [(512, 768, 768, 0.75, "fp16", "plain"), (1024, 1024, 1024, 0.5, "fp32", "plain"),
+                                             (2048, 768, 768, 0.75, "fp16", "plain"), (320, 1024, 512, 0.6, "fp32", "plain"),
+                                             (512, 768, 768, 0.75, "fp16", "bias"), (1024, 1024, 1024, 0.5, "fp32", "accum"),
+                                             (2048, 768, 768, 0.75, "fp16", "accum")])
+def test_narrow_unit_width_kernels_match_wide(tmp_path, m, k, n, s, dt, mode):
     """Small-M layers whose schedule pieces are all <= 64 / 128 tokens launch
     the narrow K2 instantiations (TB = 64 / 128, deeper pipelines).  They do
     the same per-element fp32 accumulation in the same k order as the wide
@@ -550,11 +562,21 @@ def test_narrow_unit_width_kernels_match_wide(tmp_path, m, k, n, s, dt):
     for narrow in ("1", "0"):
         f = str(tmp_path / f"ct_{narrow}.npy")
         env = dict(os.environ, TW_B200_NARROW=narrow)
-        subprocess.run([sys.executable, "-c", _NARROW_SCRIPT, root, str(m), str(k), str(n), str(s), "21", dt, f],
+        subprocess.run([sys.executable, "-c", _NARROW_SCRIPT, root, str(m), str(k), str(n), str(s), "21", dt, f, mode],
                        check=True, env=env, timeout=300)
         outs[narrow] = np.load(f)
     assert np.array_equal(outs["1"], outs["0"]), "narrow and wide K2 instantiations differ"
     a, w, p = orc.bench_inputs(m, k, n, 128, s, seed=21)
     want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), k, n))
+    pr = orc.pruned_columns(p)
+    if mode == "bias":  # relu(C + bias) in fp32, pruned columns relu(bias) (trainer.py:246-248)
+        bias = np.random.default_rng(5).standard_normal(n).astype(np.float32)
+        want = np.maximum(want + bias[:, None], 0.0)
+    elif mode == "accum":  # kept rows out + A*W, pruned rows untouched
+        base = np.random.default_rng(6).standard_normal((n, m)).astype(np.float32)
+        base = base.astype(np.float16).astype(np.float32) if dt == "fp16" else base
+        want = base + want
+        assert np.array_equal(outs["1"][pr], base[pr])
     assert rel_l2(outs["1"], want) <= RTOL
-    assert np.all(outs["1"][orc.pruned_columns(p)] == 0.0)
+    if mode == "plain":
+        assert np.all(outs["1"][pr] == 0.0)
