@@ -58,6 +58,8 @@ WORKLOADS = {
     # 512-unit LSTM layer, [x_t; h_{t-1}] (K=1024) -> 4 gates (N=2048), 4096 tokens
     "NMT": (4096, 1024, 2048, 128, 0.75, "NMT LSTM gate GEMM M=4096 K=1024 N=2048 (assumed), G=128, 75% TW"),
     # VGG-16 conv layers as im2col GEMMs at batch 64 (BASELINE config 3): M = 64*H*W
+    "VGG_conv1_1": (3211264, 27, 64, 128, 0.75, "VGG-16 conv1_1 im2col b64: M=3211264 K=27 N=64, 75% TW"),
+    "VGG_conv2_1": (802816, 576, 128, 128, 0.75, "VGG-16 conv2_1 im2col b64: M=802816 K=576 N=128, 75% TW"),
     "VGG_conv1_2": (3211264, 576, 64, 128, 0.75, "VGG-16 conv1_2 im2col b64: M=3211264 K=576 N=64, 75% TW"),
     "VGG_conv3_2": (200704, 2304, 256, 128, 0.75, "VGG-16 conv3_2 im2col b64: M=200704 K=2304 N=256, 75% TW"),
     "VGG_conv4_2": (50176, 4608, 512, 128, 0.50, "VGG-16 conv4_2 im2col b64: M=50176 K=4608 N=512, 50% TW"),

@@ -177,7 +177,7 @@ int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, c
     return TW_OK;
   }
   HostSchedule hs;
-  int rc = pair_clusters > 0 ? build_pair_schedule(p->host, m, zero_rows, pair_clusters, hs)
+  int rc = pair_clusters > 0 ? build_pair_schedule(p->host, m, ob, zero_rows, pair_clusters, hs)
                              : build_schedule(p->host, m, ob, zero_rows, sms, tokens_per_unit(p->host.block_n), hs);
   if (rc) return rc;
   if (hs.units.empty()) hs.units.assign(4, 0);
@@ -186,6 +186,8 @@ int get_schedule(const tw_plan *p, int64_t m, int ob, bool zero_rows, int sms, c
   ds.has_contig = hs.has_contig;
   ds.has_tma_rows = hs.has_tma_rows;
   ds.pair = hs.pair;
+  ds.zero_cpr = hs.zero_cpr;
+  ds.zero_chunk = hs.zero_chunk;
   // the K2 instantiation: the narrowest unit width that holds every piece
   // (narrow kernels run deeper pipelines; TW_B200_NARROW=0 keeps the wide one)
   static const bool narrow = [] {
@@ -430,6 +432,8 @@ static int gemm_impl(const tw_plan *p, const void *at, int64_t m, int64_t lda, v
   a.kidx = p->d_kidx;
   a.colids = p->d_colids;
   a.zero_rows = p->d_zero;
+  a.zero_cpr = sched->zero_cpr;
+  a.zero_chunk = sched->zero_chunk;
   a.wimg = p->d_wimg;
   a.sched = sched->units;
   a.sched_off = sched->off;

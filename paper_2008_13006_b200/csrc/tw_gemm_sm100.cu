@@ -232,17 +232,19 @@ __device__ __forceinline__ float const_row_value(const GemmArgs &a, int row) {
 // One constant row (a pruned column of C) written by one warp: coalesced
 // 16-byte streaming stores, 512 B per instruction.
 template <typename OutT, bool kPeer>
-__device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int lane, bool vec) {
-  OutT *base = reinterpret_cast<OutT *>(a.out) + (int64_t)row * a.ldc;
-  const int64_t n16 = vec ? (int64_t)a.M * (int64_t)sizeof(OutT) / 16 : 0;
+__device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int64_t t0, int64_t t1, int lane,
+                                               bool vec) {
+  OutT *base = reinterpret_cast<OutT *>(a.out) + (int64_t)row * a.ldc + t0;
+  const int64_t len = t1 - t0;  // t0 is a multiple of 64 tokens: 16-byte aligned when the row is
+  const int64_t n16 = vec ? len * (int64_t)sizeof(OutT) / 16 : 0;
   const float c = const_row_value(a, row);
   float cv[8] = {c, c, c, c, c, c, c, c};
   const uint4 z = pack16<OutT>(cv);
   for (int d = -1; d < (kPeer ? a.n_peer : 0); ++d) {  // the local output, then every peer replica
-    OutT *bd = d < 0 ? base : reinterpret_cast<OutT *>(a.peer[d]) + (int64_t)row * a.ldc;
+    OutT *bd = d < 0 ? base : reinterpret_cast<OutT *>(a.peer[d]) + (int64_t)row * a.ldc + t0;
     uint4 *b16d = reinterpret_cast<uint4 *>(bd);
     for (int64_t i = lane; i < n16; i += 32) __stcs(b16d + i, z);
-    for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < a.M; i += 32) bd[i] = cvt_out<OutT>(c);
+    for (int64_t i = n16 * 16 / (int64_t)sizeof(OutT) + lane; i < len; i += 32) bd[i] = cvt_out<OutT>(c);
   }
 }
 
@@ -250,16 +252,21 @@ __device__ __forceinline__ void write_zero_row(const GemmArgs &a, int row, int l
 // block, issued by lane 0: zero rows never occupy the LSU that the gathers
 // need (tools/membench7.cu: 8 KB bulk stores reach 5.4 TB/s chip-wide).
 // Falls back to STG when the row is not 16-byte aligned / sized.
+// One zero-row PIECE p of the schedule (HostSchedule::zero_cpr pieces per
+// row of zero_chunk tokens each).
 template <typename OutT, bool kPeer>
-__device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int row, int lane, bool bulk_ok, bool vec,
+__device__ __forceinline__ void zero_row_bulk(const GemmArgs &a, int p, int lane, bool bulk_ok, bool vec,
                                               const uint8_t *zero_buf, uint32_t zero_bytes) {
+  const int row = __ldg(a.zero_rows + p / a.zero_cpr);
+  const int64_t t0 = (int64_t)(p % a.zero_cpr) * a.zero_chunk;
+  const int64_t t1 = min((int64_t)a.M, t0 + (int64_t)a.zero_chunk);
   if (!bulk_ok || kPeer || (a.bias != nullptr && const_row_value(a, row) != 0.f)) {
-    write_zero_row<OutT, kPeer>(a, row, lane, vec);
+    write_zero_row<OutT, kPeer>(a, row, t0, t1, lane, vec);
     return;
   }
   if (lane == 0) {
-    char *dst = reinterpret_cast<char *>(a.out) + (int64_t)row * a.ldc * (int64_t)sizeof(OutT);
-    const int64_t bytes = (int64_t)a.M * (int64_t)sizeof(OutT);
+    char *dst = reinterpret_cast<char *>(a.out) + ((int64_t)row * a.ldc + t0) * (int64_t)sizeof(OutT);
+    const int64_t bytes = (t1 - t0) * (int64_t)sizeof(OutT);
     for (int64_t off = 0; off < bytes; off += zero_bytes) {
       const uint32_t n = (uint32_t)min((int64_t)zero_bytes, bytes - off);
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + off),
@@ -808,7 +815,11 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         }
       };
       const bool narrow = fast && nq * 8 < kChunks && (nq == 1 || nq == 2) && !dbg<kTrace>(args, 512);
-      if ((rec.z >> 12) & 1) {
+      // the MMA reads only the stage's first 16 * nk rows (nk = k-steps):
+      // a warp whose rows all lie beyond them (the padding of a unit's last,
+      // partial stage) issues nothing -- it still arrives on `full` below
+      const bool needed = gw * kRowsPerWarp < ((rec.z >> 4) & 0xf) * 16;
+      if (((rec.z >> 12) & 1) || !needed) {
         // consecutive kept rows: the weight warp loads them with TMA tiles
       } else if (narrow && nq == 2) {
         gather_rows(std::integral_constant<int, 2>{});
@@ -1032,7 +1043,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
         if (lane == 0 && bulk_ok) {
           if (dbg<kTrace>(args, 2048)) ptx::bulk_wait_read<2>(); else ptx::bulk_wait_read<0>();
         }
-        zero_row_bulk<OutT, kPeer>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
+        zero_row_bulk<OutT, kPeer>(args, zr, lane, bulk_ok, vec, sZero, C::kZeroBytes);
         ++zr;
       }
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -1071,7 +1082,7 @@ __global__ void __launch_bounds__(kThreads, 1) tw_gemm_sm100_kernel(const __grid
     if (e == 0 && lane == 0) *s_zdone = zr;
     epi_sync();
     for (zr = *s_zdone + e; zr < z1; zr += kEpiWarps)
-      zero_row_bulk<OutT, kPeer>(args, __ldg(args.zero_rows + zr), lane, bulk_ok, vec, sZero, C::kZeroBytes);
+      zero_row_bulk<OutT, kPeer>(args, zr, lane, bulk_ok, vec, sZero, C::kZeroBytes);
     // before exit the bulk stores must have READ shared memory (it is
     // released with the CTA); their global writes complete with the grid
     // (the same contract as CUTLASS's TMA-store epilogues)
@@ -1251,7 +1262,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __
       if (et < 128) ucol[et] = (tile >= 0 && et < t.n_i) ? __ldg(args.colids + t.col_off + et) : -1;
       while (e == 0 && zr < z1 && !ptx::mbar_test_wait(&tfull[acc], use[acc] & 1)) {
         if (lane == 0) ptx::bulk_wait_read<0>();
-        zero_row_bulk<OutT, false>(args, __ldg(args.zero_rows + zr), lane, true, true, sZero, 8192);
+        zero_row_bulk<OutT, false>(args, zr, lane, true, true, sZero, 8192);
         ++zr;
       }
       ptx::mbar_wait(&tfull[acc], use[acc] & 1);
@@ -1280,7 +1291,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) tw_pair_sm100_kernel(const __
     if (e == 0 && lane == 0) *s_zdone = zr;
     epi_sync();
     for (zr = *s_zdone + e; zr < z1; zr += 8)
-      zero_row_bulk<OutT, false>(args, __ldg(args.zero_rows + zr), lane, true, true, sZero, 8192);
+      zero_row_bulk<OutT, false>(args, zr, lane, true, true, sZero, 8192);
     if (lane == 0) ptx::bulk_wait_read<0>();
   }
 

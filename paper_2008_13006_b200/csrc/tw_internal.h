@@ -80,6 +80,13 @@ struct HostSchedule {
   bool has_tma_rows = false;   // some unit's tile has 128 consecutive output rows (unit flag bit 1)
   bool pair = false;           // K4 (CTA-pair) schedule: off is per cluster, no stage stream
   int max_nq = 0;              // widest half (64-token quarters) of any unit
+  // zero rows are scheduled as PIECES of zero_chunk tokens (zero_cpr pieces
+  // per row; piece p = row zero_rows[p / zero_cpr], tokens from
+  // (p % zero_cpr) * zero_chunk): a pruned column of a long layer (VGG conv1:
+  // 6.4 MB per row) spreads over many CTAs instead of landing on one; zoff
+  // counts pieces
+  int32_t zero_cpr = 1;
+  int32_t zero_chunk = 0;
   double makespan_ns = 0, mean_ns = 0;
 };
 int build_schedule(const HostPlan &hp, int64_t m, int out_bytes, bool zero_rows, int sms, int tb,
@@ -91,7 +98,7 @@ bool pair_eligible(const HostPlan &hp);
 // token, consecutive-rows flags (bit r: rank r's tile owns 128 consecutive
 // C^T rows)} of 256 tokens, dealt round-robin to `clusters` CTA pairs
 // (off: clusters + 1); zero rows split evenly over the 2 * clusters CTAs.
-int build_pair_schedule(const HostPlan &hp, int64_t m, bool zero_rows, int clusters, HostSchedule &s);
+int build_pair_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int clusters, HostSchedule &s);
 
 constexpr int kParamCtas = 160;
 
@@ -101,6 +108,8 @@ struct GemmArgs {
   const int32_t *kidx;
   const int32_t *colids;
   const int32_t *zero_rows;
+  int32_t zero_cpr;    // zero-row pieces per row (HostSchedule::zero_cpr)
+  int32_t zero_chunk;  // tokens per zero-row piece
   const uint8_t *wimg;
   const int4 *sched;         // per-CTA unit lists (HostSchedule::units)
   const int32_t *sched_off;  // grid + 1
@@ -156,6 +165,7 @@ struct tw_dev_schedule {
   bool has_contig = false;
   bool has_tma_rows = false;
   bool pair = false;  // K4 schedule (grid = 2 x clusters)
+  int32_t zero_cpr = 1, zero_chunk = 0;  // zero-row pieces (HostSchedule)
   int tb = 256;       // K2 unit width the launch instantiates (64 / 128 / 256 tokens)
   std::vector<int32_t> h_off, h_soff, h_zoff;  // host copies (kernel-parameter offsets)
   int4 *units = nullptr;

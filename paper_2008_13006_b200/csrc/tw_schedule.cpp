@@ -112,12 +112,32 @@ std::vector<int64_t> water_fill(const std::vector<double> &load, int64_t rows, d
   return z;
 }
 
+// Zero-row pieces: rows of more than kZeroPieceBytes are cut into pieces of
+// equal token ranges (multiples of 64 tokens) so the water-fill can spread
+// one long row over many CTAs.  Sets s.zero_cpr / s.zero_chunk; returns the
+// number of pieces.
+constexpr int64_t kZeroPieceBytes = 256 << 10;
+
+int64_t zero_pieces(int64_t rows, int64_t m, int ob, HostSchedule &s) {
+  int64_t cpr = std::max<int64_t>(1, (m * ob + kZeroPieceBytes - 1) / kZeroPieceBytes);
+  int64_t chunk = (m + cpr - 1) / cpr;
+  chunk = (chunk + 63) / 64 * 64;
+  cpr = std::max<int64_t>(1, (m + chunk - 1) / chunk);
+  while (rows * cpr > INT32_MAX / 2) {  // (huge layers) coarser pieces
+    chunk *= 2;
+    cpr = (m + chunk - 1) / chunk;
+  }
+  s.zero_cpr = (int32_t)cpr;
+  s.zero_chunk = (int32_t)std::min<int64_t>(chunk, INT32_MAX);
+  return rows * cpr;
+}
+
 }  // namespace
 
 int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sms, int tb, HostSchedule &s) {
   s = HostSchedule{};
-  const int64_t Z = zero_rows ? (int64_t)hp.zero_rows.size() : 0;
-  const double zc = (double)m * ob / kWriteBps;
+  const int64_t Z = zero_pieces(zero_rows ? (int64_t)hp.zero_rows.size() : 0, m, ob, s);
+  const double zc = (double)std::min<int64_t>(m, s.zero_chunk) * ob / kWriteBps;
   const int qmax = 2 * tb / 64;  // quarters per piece (two halves of tb tokens)
   const int64_t q_tile = (m + 63) / 64;
   auto by_cost = [](const Unit &a, const Unit &b) {
@@ -140,7 +160,7 @@ int build_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int sm
     std::stable_sort(u.begin(), u.end(), by_cost);
     return u;
   };
-  const int64_t zero_ctas = Z > 0 ? (Z * m * ob + (256 << 10) - 1) / (256 << 10) : 0;
+  const int64_t zero_ctas = Z > 0 ? (Z * std::min<int64_t>(m, s.zero_chunk) * ob + (256 << 10) - 1) / (256 << 10) : 0;
   // CTAs: enough for every piece of one quarter, so small layers (fewer
   // pieces than SMs) can spread over more SMs
   const int64_t quarters = q_tile * (int64_t)hp.tiles.size();
@@ -294,7 +314,7 @@ bool pair_eligible(const HostPlan &hp) {
   return true;
 }
 
-int build_pair_schedule(const HostPlan &hp, int64_t m, bool zero_rows, int clusters, HostSchedule &s) {
+int build_pair_schedule(const HostPlan &hp, int64_t m, int ob, bool zero_rows, int clusters, HostSchedule &s) {
   s = HostSchedule{};
   const int L = (int)hp.tiles.size();
   const int P = (L + 1) / 2;
@@ -332,7 +352,7 @@ int build_pair_schedule(const HostPlan &hp, int64_t m, bool zero_rows, int clust
     s.units.insert(s.units.end(), per[(size_t)c].begin(), per[(size_t)c].end());
     s.off[(size_t)c + 1] = (int32_t)(s.units.size() / 4);
   }
-  const int64_t Z = zero_rows ? (int64_t)hp.zero_rows.size() : 0;
+  const int64_t Z = zero_pieces(zero_rows ? (int64_t)hp.zero_rows.size() : 0, m, ob, s);
   s.zoff.assign((size_t)s.grid + 1, 0);
   for (int c = 0; c < s.grid; ++c) s.zoff[(size_t)c + 1] = (int32_t)(Z * (c + 1) / s.grid);
   s.soff.assign((size_t)s.grid + 1, 0);

@@ -580,3 +580,26 @@ def test_narrow_unit_width_kernels_match_wide(tmp_path, m, k, n, s, dt, mode):
     assert rel_l2(outs["1"], want) <= RTOL
     if mode == "plain":
         assert np.all(outs["1"][pr] == 0.0)
+
+
+@pytest.mark.parametrize("m,dt", [(140_000, torch.float32), (140_003, torch.float16), (262_144, torch.float16)])
+def test_long_rows_zero_pieces(m, dt):
+    """Long layers (VGG conv1: a pruned column is a 6.4 MB C^T row) schedule
+    their zero rows as pieces of <= 256 KB spread over the CTAs.  Output
+    pre-filled with NaN: every pruned row must come back exactly 0 over its
+    whole length (piece boundaries, the ragged tail, the non-bulk STG path
+    when M * 2 bytes is not a multiple of 16), kept rows within the bar."""
+    k, n, g, s = 64, 256, 128, 0.75
+    a, w, p = orc.bench_inputs(m, k, n, g, s, seed=31)
+    plan = tw.TwPlan(tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p)), dense_pad=False)
+    _, _, zoff = plan.schedule(m, "fp32" if dt == torch.float32 else "fp16")
+    pr = orc.pruned_columns(p)
+    assert len(pr) > 0 and zoff[-1] > len(pr), "expected several zero pieces per pruned row"
+    at = device_at(a)
+    out = torch.full((n, m), float("nan"), dtype=dt, device="cuda")
+    plan.gemm(at, out=out, out_dtype=dt)
+    got = out.float().cpu().numpy()
+    assert np.all(got[pr] == 0.0)
+    want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), k, n),
+                          threads=orc.max_threads())
+    assert rel_l2(got, want) <= RTOL
