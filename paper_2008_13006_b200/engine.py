@@ -180,7 +180,9 @@ class PackedPlan:
     def schedule(self, m: int, out_dtype: str = "fp32", sms: int = 148, accumulate: bool = False):
         """The static launch schedule tw_gemm uses for M tokens: per-CTA unit
         lists ((live tile, first token, 64-token quarters) rows) and zero-row
-        ranges.  Host-side; returns (units[n,4], unit_off[G+1], zero_off[G+1])."""
+        ranges.  Zero rows are counted in pieces of <= 256 KB of one row (a
+        long row is split over CTAs), so zero_off[-1] >= the number of pruned
+        rows.  Host-side; returns (units[n,4], unit_off[G+1], zero_off[G+1])."""
         code = {"fp32": _lib.TW_F32, "bf16": _lib.TW_BF16, "fp16": _lib.TW_F16}[out_dtype]
         res = []
         for which in (0, 1, 2):
