@@ -123,7 +123,7 @@ int64_t zero_pieces(int64_t rows, int64_t m, int ob, HostSchedule &s) {
   int64_t chunk = (m + cpr - 1) / cpr;
   chunk = (chunk + 63) / 64 * 64;
   cpr = std::max<int64_t>(1, (m + chunk - 1) / chunk);
-  while (rows * cpr > INT32_MAX / 2) {  // (huge layers) coarser pieces
+  while (cpr > 1 && rows * cpr > INT32_MAX / 2) {  // (huge layers) coarser pieces
     chunk *= 2;
     cpr = (m + chunk - 1) / chunk;
   }
