@@ -291,3 +291,30 @@ def test_reference_engine_task_api_names():
     groups = tw.group_by_shape([mk(0, 4, 8), mk(1, 9, 16), mk(2, 4, 16), mk(3, 30, 8)])
     assert [g.n_i for g in groups] == [8, 16] and [t.index for t in groups[0].tasks] == [0, 3]
     assert groups[0].flops == 2 * 7 * (4 * 8 + 30 * 8)
+
+
+@pytest.mark.parametrize("m,dt", [(4096, "fp16"), (140_000, "fp32"), (3_211_264, "fp16"), (802_816, "fp32")])
+def test_zero_rows_scheduled_in_balanced_pieces(m, dt):
+    """Zero rows (pruned output columns) are scheduled as pieces of <= 256 KB
+    of one C^T row (64-token multiples, tw_schedule.cpp zero_pieces), so a
+    long layer's pruned columns spread over the CTAs: the piece count is
+    rows x pieces-per-row, and no CTA gets more than a couple of pieces above
+    the lightest one (whole 6.4 MB rows landed on 32 of 148 CTAs before)."""
+    from paper_2008_13006_b200.engine import PackedPlan
+
+    k, n = 64, 256
+    _, w, p = orc.bench_inputs(8, k, n, 128, 0.75, seed=3)
+    pp = PackedPlan(tw.compact(tw.DenseMatrix.from_array(w), tw.TilePattern(k, n, 128, tuple(
+        tw.Tile(c, keep) for c, keep in p[3]))))
+    rows = len(orc.pruned_columns(p))
+    ob = 4 if dt == "fp32" else 2
+    cpr = max(1, -(-m * ob // (256 << 10)))
+    chunk = -(-(-(-m // cpr)) // 64) * 64
+    cpr = max(1, -(-m // chunk))
+    units, uoff, zoff = pp.schedule(m, dt)
+    assert zoff[0] == 0 and np.all(np.diff(zoff) >= 0)
+    assert zoff[-1] == rows * cpr
+    assert chunk * ob <= (256 << 10) + 64 * ob
+    per = np.diff(zoff)
+    if cpr > 1:
+        assert per.max() - per.min() <= max(2, per.max() // 4)
