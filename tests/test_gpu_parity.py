@@ -603,3 +603,48 @@ def test_long_rows_zero_pieces(m, dt):
     want = orc.gemm_tw_ct(np.ascontiguousarray(a.T), orc.PackedTiles(orc.compact(w, p), k, n),
                           threads=orc.max_threads())
     assert rel_l2(got, want) <= RTOL
+
+
+_FULL_SHAPES = [  # BASELINE configs at their full sizes
+    ("C5@0", 16384, 1024, 4096, 0.0, torch.float16),
+    ("C5@0.5", 16384, 1024, 4096, 0.5, torch.float16),
+    ("C5@0.75", 16384, 1024, 4096, 0.75, torch.float16),
+    ("C5@0.9", 16384, 1024, 4096, 0.9, torch.float32),
+    ("NMT@0.75", 4096, 1024, 2048, 0.75, torch.float16),
+    ("VGG conv1_1@0.75", 3211264, 27, 64, 0.75, torch.float16),
+    ("VGG conv1_2@0.5", 3211264, 576, 64, 0.5, torch.float16),
+    ("VGG conv2_1@0.75", 802816, 576, 128, 0.75, torch.float32),
+    ("VGG conv3_2@0.5", 200704, 2304, 256, 0.5, torch.float16),
+    ("VGG conv4_2@0.5", 50176, 4608, 512, 0.5, torch.float32),
+    ("VGG conv5_1@0.75", 12544, 4608, 512, 0.75, torch.float16),
+]
+
+
+@pytest.mark.parametrize("name,m,k,n,s,odt", _FULL_SHAPES, ids=[c[0] for c in _FULL_SHAPES])
+def test_full_size_integer_data_exact(name, m, k, n, s, odt):
+    """A size-independent property at the BASELINE full sizes. With integer
+    operands (A^T in {-1, 0, 1}, W in {-2 .. 2}) every product and partial
+    sum is exact in fp32 whatever the summation order, so the TW-GEMM must
+    equal the dense product with the pruned weights zeroed -- gemm_tw ==
+    gemm_dense(a, zero_fill(b, p)) (engine.py:152-164, pattern.py:244-250) --
+    EXACTLY, over every token of the layer, and a 16-bit output must be that
+    exact value rounded once.  This holds whichever kernel the call runs (K2
+    gathers / K4 dense-padded pairs), whatever unit width and zero-row
+    piecing its schedule uses.  Checker: torch.mm in fp32 on the same
+    integers (exact: |sums| <= 2K << 2^24)."""
+    p = orc.random_uniform_pattern(k, n, 128, s, 42)
+    w = np.random.default_rng(11).integers(-2, 3, size=(k, n)).astype(np.float32)
+    plan = tw.TwPlan(tw.compact(tw.DenseMatrix.from_array(w), to_tw_pattern(p)))
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    at = torch.randint(-1, 2, (k, m), device="cuda", generator=gen, dtype=torch.int8).to(torch.bfloat16)
+    ct = plan.gemm(at, out_dtype=odt)
+    wzt = torch.from_numpy(np.ascontiguousarray(orc.zero_fill(w, p).T)).cuda()  # N x K
+    ref = torch.empty((n, m), dtype=torch.float32, device="cuda")
+    step = 1 << 19
+    for t0 in range(0, m, step):
+        ref[:, t0:t0 + step] = wzt @ at[:, t0:t0 + step].float()
+    assert torch.equal(ct, ref.to(odt)), f"{name}: TW-GEMM differs from the exact dense product"
+    pr = torch.from_numpy(orc.pruned_columns(p).astype(np.int64)).cuda()
+    assert bool((ct.index_select(0, pr) == 0).all())
+    del at, ct, ref
+    torch.cuda.empty_cache()
